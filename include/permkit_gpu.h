@@ -1,0 +1,143 @@
+/*
+ * permkit_gpu.h — C ABI of the B200-native Gray-code Ryser/Glynn engine.
+ *
+ * This is the drop-in boundary for the reference package's hot path
+ * (arxiv/paper_2602_10141, package `permkit`).  The reference evaluates
+ * permanents by walking Gray-code blocks in numba kernels selected per block
+ * by engine._run_plan; this library replaces those walks with sm_100a CUDA
+ * kernels and takes one call per range / batch / prime set instead of one
+ * call per block.  All entry points:
+ *   - are extern "C", take plain pointers and sizes (no torch/numpy types),
+ *   - read caller buffers during the call only (nothing is retained),
+ *   - return 0 on success or a negative status (see PK_ERR_*), with a
+ *     message available from pk_last_error() on the calling thread,
+ *   - are reentrant; concurrent calls on one device are serialised.
+ *
+ * Matrix layout: row-major n x n; complex matrices are interleaved
+ * (re, im) float64 pairs, i.e. exactly numpy complex128 memory.
+ * Gray index space: [0, 2^m), m = n (Ryser) or n - 1 (Glynn); index b
+ * denotes the subset / sign vector gray(b) = b ^ (b >> 1)
+ * (reference pkg/src/permkit/gray.py:19-31).
+ */
+#ifndef PERMKIT_GPU_H
+#define PERMKIT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PK_OK 0
+#define PK_ERR_CUDA (-1)     /* CUDA runtime / launch failure                 */
+#define PK_ERR_ARG (-2)      /* invalid argument (shape, range, modulus, ...)  */
+#define PK_ERR_LIMIT (-3)    /* documented capability limit exceeded           */
+#define PK_ERR_INTERNAL (-4)
+
+#define PK_ALGO_RYSER 0
+#define PK_ALGO_GLYNN 1
+
+/* Message for the last failing call made by this thread ("" if none). */
+const char* pk_last_error(void);
+
+/* Number of visible CUDA devices (>= 0), or a negative status. */
+int pk_device_count(void);
+
+/* Library version, e.g. 100 for 0.1.0. */
+int pk_version(void);
+
+/* Largest n the register-resident production kernels accept (48). */
+int pk_max_n(void);
+
+/*
+ * fp64 walk of ONE matrix over the Gray range [start, start + length).
+ * Replaces kernels.ryser_partial / kernels.glynn_partial
+ * (reference pkg/src/permkit/kernels.py:415-430) and the per-block thread
+ * pool of engine._run_plan (engine.py:213-245) for COMPLEX / REAL domains.
+ *   out[4]  = {sum_re, sum_im, comp_re, comp_im}: a compensated pair whose
+ *             value sum + comp is the signed partial sum (Glynn unscaled,
+ *             as glynn_partial returns it); im parts are 0 for real input.
+ *   abs_sum = optional (may be NULL): sum of |re t| + |im t| over the terms,
+ *             an upper bound of sum |t| used by the parity tolerance.
+ *   ndev    = devices to split the range over (clamped to the device count).
+ * The aligned interior runs in the register-resident production kernel; an
+ * unaligned head/tail is walked with the reference's exact arithmetic.
+ * The result for a given (a, start, length) is deterministic and, for
+ * power-of-two ndev, identical for every ndev.
+ */
+int pk_ryser_f64(const double* a, int n, int is_complex, int algo, uint64_t start,
+                 uint64_t length, int ndev, double out[4], double* abs_sum);
+
+/*
+ * Bit-exact parity mode: one GPU thread walks each caller block exactly as
+ * the reference's numba kernel does (no FMA, same operation order,
+ * Neumaier per component).  out[4*i .. 4*i+3] = {s_re, s_im, c_re, c_im} of
+ * block i, bit-identical to kernels.ryser_partial(a, starts[i], lens[i])
+ * (kernels.py:33-123) or glynn_partial (kernels.py:126-226).  n <= 64.
+ */
+int pk_ryser_f64_blocks(const double* a, int n, int is_complex, int algo,
+                        const uint64_t* starts, const uint64_t* lens, int nblocks, int device,
+                        double* out);
+
+/*
+ * Full-range permanents of B matrices (contiguous B x n x n), e.g. the
+ * ensemble sampler (ensembles.py:142-158) and the geodesic sweep
+ * (geodesics.py:153-179).  out[4*b ..] as in pk_ryser_f64 for matrix b;
+ * abs_sums[b] optional.  Matrices are split over ndev devices.
+ */
+int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex, int algo, int ndev,
+                       double* out, double* abs_sums);
+
+/*
+ * F_p walk over [start, start + length) for P moduli at once.
+ *   a      = P x n x n residues, a[k][i][j] in [0, primes[k])
+ *   primes = P moduli, each 2 <= p < 2^62 (PrimeField range, domains.py:126-130)
+ *   out[k] = exact signed walk sum over the range mod primes[k], in [0, p):
+ *            the value sum(kernels.ryser_partial_modp(a_k, blk...)) mod p
+ *            (kernels.py:250-290, 433-434); Glynn is NOT scaled by 2^(1-n).
+ * Odd p < 2^31 run in the Montgomery-32 production kernel with up to four
+ * primes per lane; other moduli use the generic 64-bit walker.
+ */
+int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, int n, int algo,
+                  uint64_t start, uint64_t length, int ndev, uint64_t* out);
+
+/*
+ * Resident jobs for measurement (bench.py): the matrix / residues are
+ * uploaded once and the walk is re-run on device-resident inputs.  The range
+ * must be aligned to the job's tile span (any full range is).
+ */
+typedef struct pk_job pk_job;
+
+int pk_job_f64_create(int device, const double* a, int n, int is_complex, int algo,
+                      uint64_t start, uint64_t length, pk_job** job);
+int pk_job_modp_create(int device, const uint64_t* a, const uint64_t* primes, int P, int n,
+                       int algo, uint64_t start, uint64_t length, pk_job** job);
+/*
+ * Run `iters` walks back to back on the job's stream.  Between iterations a
+ * buffer of flush_bytes is overwritten (L2 flush; 0 = none).  total_ms =
+ * device time of the whole sequence (CUDA events, includes flushes);
+ * walk_ms = summed device time of the walk kernel launches only.
+ * out_f64[5] = (s_re, c_re, s_im, c_im, abs) of the last run (f64 jobs);
+ * out_res[P] = residues of the last run (F_p jobs).  Either may be NULL.
+ */
+int pk_job_run(pk_job* job, int iters, size_t flush_bytes, double* total_ms, double* walk_ms,
+               double* out_f64, uint64_t* out_res);
+/* info[0..7] = k (segment bits), tiles, grid CTAs, CTAs per SM, registers per
+ * thread, local (spill) bytes, dynamic smem bytes, kernel launches per run. */
+int pk_job_info(pk_job* job, int64_t* info);
+void pk_job_destroy(pk_job* job);
+
+/*
+ * Pipe-rate micro-benchmarks (roofline denominators).  Fills out[3*i..] =
+ * {lane-ops/s, lane-ops per SM clock, mean SM MHz} for the ops named by
+ * pk_peak_names() (comma separated).  Returns the number of ops measured.
+ */
+int pk_measure_peaks(int device, double* out, int max_out);
+const char* pk_peak_names(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PERMKIT_GPU_H */

@@ -1,0 +1,1024 @@
+// Host orchestration and the extern "C" boundary (include/permkit_gpu.h).
+//
+// Replaces, for the GPU build, the execution half of the reference engine:
+//   engine._run_plan's fast branches (reference engine.py:213-258): per-block
+//     numba calls on a ThreadPoolExecutor + ordered Kahan combine
+//   the per-sample / per-t / per-prime pools of ensembles.sample_permanents
+//     (ensembles.py:142-158), geodesics.sweep (geodesics.py:153-179) and
+//     modular.schur_permanent_exact (modular.py:188-206)
+// with: one host thread per GPU, a persistent walk kernel per device, a
+// deterministic device-side tree reduction, and a host combine of <= 8 roots.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <utility>
+
+#include "../../include/permkit_gpu.h"
+#include "pk_block.cuh"
+#include "pk_common.cuh"
+#include "pk_reduce.cuh"
+#include "pk_registry.h"
+#include "pk_walk.cuh"
+
+namespace pk {
+
+// ---------------------------------------------------------------------------
+// errors
+
+namespace {
+thread_local std::string g_last_error;
+}
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+#define PK_REQUIRE(cond, code, msg) \
+  do {                              \
+    if (!(cond)) fail((code), (msg)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// kernel tables
+
+struct Tables {
+  const void* f64[2][kMaxN + 1] = {};
+  const void* modp[2][kMaxP + 1][kMaxN + 1] = {};  // [lazy][P][N]
+};
+
+static const Tables& tables() {
+  static const Tables t = [] {
+    Tables t;
+#define PK_REG(lo, hi)                       \
+  register_f64_c0_##lo(t.f64[0]);            \
+  register_f64_c1_##lo(t.f64[1]);            \
+  register_modp_l0_p1_##lo(t.modp[0][1]);   \
+  register_modp_l0_p2_##lo(t.modp[0][2]);   \
+  register_modp_l0_p3_##lo(t.modp[0][3]);   \
+  register_modp_l0_p4_##lo(t.modp[0][4]);   \
+  register_modp_l1_p1_##lo(t.modp[1][1]);   \
+  register_modp_l1_p2_##lo(t.modp[1][2]);   \
+  register_modp_l1_p3_##lo(t.modp[1][3]);   \
+  register_modp_l1_p4_##lo(t.modp[1][4]);
+    PK_FOR_EACH_RANGE(PK_REG)
+#undef PK_REG
+    return t;
+  }();
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// per-device context
+
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) PK_CUDA(cudaFree(p));
+      p = nullptr;
+      cap = 0;
+      PK_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+      cap = std::max<size_t>(bytes, 256);
+    }
+    return p;
+  }
+};
+
+struct DevCtx {
+  int dev = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  DBuf a, partials, out, primes, starts, lens, blockout, blockabs, modp_out;
+  std::map<std::pair<const void*, int>, int> occ;  // (kernel, smem) -> CTAs per SM
+};
+
+static std::mutex g_ctx_mu;
+static DevCtx* g_ctx[64] = {};
+
+static int device_count() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    cudaGetLastError();
+    return 0;
+  }
+  PK_CUDA(e);
+  return n;
+}
+
+static DevCtx& ctx(int dev) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  PK_REQUIRE(dev >= 0 && dev < 64, kErrArg, "device index out of range");
+  if (!g_ctx[dev]) {
+    const int nd = device_count();
+    PK_REQUIRE(dev < nd, kErrArg,
+               "CUDA device " + std::to_string(dev) + " not available (" + std::to_string(nd) +
+                   " visible)");
+    auto* c = new DevCtx;
+    c->dev = dev;
+    PK_CUDA(cudaSetDevice(dev));
+    PK_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
+    PK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    g_ctx[dev] = c;
+  }
+  return *g_ctx[dev];
+}
+
+static int occupancy(DevCtx& c, const void* fn, int threads, int smem) {
+  auto key = std::make_pair(fn, smem);
+  auto it = c.occ.find(key);
+  if (it != c.occ.end()) return it->second;
+  if (smem > 48 * 1024) {
+    PK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
+  int nb = 0;
+  PK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
+  PK_REQUIRE(nb > 0, kErrLimit,
+             "walk kernel does not fit on an SM (shared memory " + std::to_string(smem) + " B)");
+  c.occ[key] = nb;
+  return nb;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+
+struct Plan {
+  int n = 0, m = 0, k = 0;   // k = 0: no aligned tiles (tiny m), everything ragged
+  uint64_t tiles_total = 0;  // aligned tiles per matrix over the whole range
+  uint64_t group = 1;        // tiles per reduction group (global alignment)
+  int piece_bits = 10;       // ragged pieces are aligned to 2^piece_bits
+};
+
+static int ilog2_floor(double x) { return x < 1 ? 0 : static_cast<int>(std::floor(std::log2(x))); }
+
+static Plan make_plan(int n, int algo, int B) {
+  Plan p;
+  p.n = n;
+  p.m = algo == PK_ALGO_RYSER ? n : n - 1;
+  const int m = p.m;
+  if (m < 6) {
+    p.k = 0;
+    p.piece_bits = std::max(m, 1);
+    return p;
+  }
+  const int kmin = std::min(m - 5, 8);
+  if (B <= 1) {
+    p.k = std::max(kmin, m - 22);
+  } else {
+    const int t = std::clamp(ilog2_floor(double(1 << 17) / B), 0, m - 5 - kmin);
+    p.k = m - 5 - t;
+  }
+  p.tiles_total = 1ull << (m - p.k - 5);
+  p.group = std::max<uint64_t>(1, p.tiles_total / kMaxGroups);
+  p.piece_bits = std::min(p.k, 10);
+  return p;
+}
+
+struct Range {
+  uint64_t start, end;         // [start, end)
+  uint64_t t0 = 0, t1 = 0;     // aligned tiles [t0, t1)
+  std::vector<std::pair<uint64_t, uint64_t>> head, tail;  // (start, len) pieces
+};
+
+static void split_pieces(uint64_t s, uint64_t e, int bits,
+                         std::vector<std::pair<uint64_t, uint64_t>>& out) {
+  const uint64_t span = 1ull << bits;
+  while (s < e) {
+    const uint64_t nxt = std::min(e, (s / span + 1) * span);
+    out.emplace_back(s, nxt - s);
+    s = nxt;
+  }
+}
+
+static Range make_range(const Plan& p, uint64_t start, uint64_t length) {
+  Range r;
+  r.start = start;
+  r.end = start + length;
+  if (length == 0) return r;
+  if (p.k == 0) {
+    split_pieces(r.start, r.end, p.piece_bits, r.head);
+    return r;
+  }
+  const int tb = p.k + 5;
+  const uint64_t ts = 1ull << tb;
+  const uint64_t A = (start + ts - 1) / ts * ts, Bt = r.end / ts * ts;
+  if (A < Bt) {
+    r.t0 = A >> tb;
+    r.t1 = Bt >> tb;
+    split_pieces(r.start, A, p.piece_bits, r.head);
+    split_pieces(Bt, r.end, p.piece_bits, r.tail);
+  } else {
+    split_pieces(r.start, r.end, p.piece_bits, r.head);
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// fp64 device work
+
+struct Node {
+  Pair re{0, 0}, im{0, 0};
+  double ab = 0;
+};
+static Node node_combine_h(const Node& a, const Node& b) {
+  return Node{pair_combine(a.re, b.re), pair_combine(a.im, b.im), a.ab + b.ab};
+}
+static Node node_from5(const double* v) { return Node{Pair{v[0], v[1]}, Pair{v[2], v[3]}, v[4]}; }
+
+// Enqueue walk + reduce for matrices already on the device.  Returns the
+// number of kernel launches.  d_out receives [B][5] roots.
+struct F64Launch {
+  const void* fn;
+  int grid, smem, per_warp, occ;
+  WalkArgs args;
+};
+
+static F64Launch prepare_f64(DevCtx& c, const Plan& p, bool cplx, int algo, int B,
+                             const double* d_a, uint64_t t0, uint64_t nt, bool want_abs,
+                             double* d_partials) {
+  PK_REQUIRE(p.n >= 1 && p.n <= kMaxN, kErrLimit,
+             "dimension " + std::to_string(p.n) + " exceeds the GPU kernel range n <= " +
+                 std::to_string(kMaxN));
+  F64Launch L{};
+  L.fn = tables().f64[cplx ? 1 : 0][p.n];
+  PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing fp64 kernel instantiation");
+  L.per_warp = B > 1 ? 1 : 0;
+  const int elem = cplx ? 16 : 8;
+  const int slot = (p.n + p.n * p.m) * elem;
+  L.smem = slot * (L.per_warp ? kWalkWarps : 1);
+  L.occ = occupancy(c, L.fn, kWalkThreads, L.smem);
+  const uint64_t units = static_cast<uint64_t>(B) * nt;
+  const uint64_t ctas = (units + kWalkWarps - 1) / kWalkWarps;
+  L.grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(c.sms) * L.occ));
+  WalkArgs& a = L.args;
+  a.a = d_a;
+  a.B = B;
+  a.n = p.n;
+  a.m = p.m;
+  a.algo = algo;
+  a.k = p.k;
+  a.per_warp_slot = L.per_warp;
+  a.tile0 = t0;
+  a.tiles = nt;
+  a.segs_total = 1ull << (p.m - p.k);
+  a.partials = d_partials;
+  a.modp_out = nullptr;
+  a.primes = nullptr;
+  a.want_abs = want_abs ? 1 : 0;
+  return L;
+}
+
+static void launch_walk(DevCtx& c, const void* fn, int grid, int smem, WalkArgs& args) {
+  void* kargs[] = {&args};
+  PK_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kWalkThreads), kargs, smem, c.stream));
+}
+
+static void launch_reduce(DevCtx& c, const double* d_partials, int B, uint64_t t0, uint64_t nt,
+                          uint64_t group, double* d_out) {
+  const uint64_t g0 = t0 / group, g1 = (t0 + nt - 1) / group + 1;
+  PK_REQUIRE(g1 - g0 <= static_cast<uint64_t>(kMaxGroups) + 1, kErrInternal,
+             "too many reduction groups");
+  reduce_tiles_kernel<<<B, kReduceThreads, 0, c.stream>>>(d_partials, t0, nt, group, d_out);
+  PK_CUDA(cudaGetLastError());
+}
+
+// exact-arithmetic pieces on one device; returns one Node per piece
+static std::vector<Node> run_f64_pieces(DevCtx& c, const double* d_a, int n, bool cplx, int algo,
+                                        const std::vector<std::pair<uint64_t, uint64_t>>& pieces,
+                                        bool want_abs) {
+  std::vector<Node> res(pieces.size());
+  if (pieces.empty()) return res;
+  const int np = static_cast<int>(pieces.size());
+  std::vector<uint64_t> hs(np), hl(np);
+  for (int i = 0; i < np; ++i) {
+    hs[i] = pieces[i].first;
+    hl[i] = pieces[i].second;
+  }
+  auto* ds = static_cast<uint64_t*>(c.starts.get(np * 8));
+  auto* dl = static_cast<uint64_t*>(c.lens.get(np * 8));
+  auto* dout = static_cast<double*>(c.blockout.get(np * 4 * 8));
+  auto* dabs = static_cast<double*>(c.blockabs.get(np * 8));
+  PK_CUDA(cudaMemcpyAsync(ds, hs.data(), np * 8, cudaMemcpyHostToDevice, c.stream));
+  PK_CUDA(cudaMemcpyAsync(dl, hl.data(), np * 8, cudaMemcpyHostToDevice, c.stream));
+  const int grid = (np + kBlockThreads - 1) / kBlockThreads;
+  double* ab = want_abs ? dabs : nullptr;
+  if (cplx) {
+    if (algo == 0)
+      block_f64_kernel<true, 0><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab);
+    else
+      block_f64_kernel<true, 1><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab);
+  } else {
+    if (algo == 0)
+      block_f64_kernel<false, 0><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab);
+    else
+      block_f64_kernel<false, 1><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab);
+  }
+  PK_CUDA(cudaGetLastError());
+  std::vector<double> h(np * 4), habs(np, 0.0);
+  PK_CUDA(cudaMemcpyAsync(h.data(), dout, np * 4 * 8, cudaMemcpyDeviceToHost, c.stream));
+  if (want_abs)
+    PK_CUDA(cudaMemcpyAsync(habs.data(), dabs, np * 8, cudaMemcpyDeviceToHost, c.stream));
+  PK_CUDA(cudaStreamSynchronize(c.stream));
+  for (int i = 0; i < np; ++i)
+    res[i] = Node{Pair{h[4 * i], h[4 * i + 2]}, Pair{h[4 * i + 1], h[4 * i + 3]}, habs[i]};
+  return res;
+}
+
+// Run `fn(dev_index)` on devices [0, ndev) with one host thread per device.
+template <class F>
+static void for_devices(int ndev, F&& fn) {
+  if (ndev <= 1) {
+    fn(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  std::vector<std::string> err(ndev);
+  std::vector<int> code(ndev, 0);
+  for (int d = 0; d < ndev; ++d) {
+    th.emplace_back([&, d] {
+      try {
+        fn(d);
+      } catch (const Error& e) {
+        err[d] = e.what();
+        code[d] = e.code;
+      } catch (const std::exception& e) {
+        err[d] = e.what();
+        code[d] = kErrInternal;
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int d = 0; d < ndev; ++d)
+    if (code[d]) fail(code[d], "device " + std::to_string(d) + ": " + err[d]);
+}
+
+static int clamp_ndev(int ndev) {
+  const int nd = device_count();
+  PK_REQUIRE(nd > 0, kErrCuda, "no CUDA device visible");
+  return std::max(1, std::min(ndev, nd));
+}
+
+// Binary tree over device roots (power-of-two count), else ordered fold.
+static Node combine_roots(const std::vector<Node>& v) {
+  std::vector<Node> cur = v;
+  const size_t n = cur.size();
+  if (n && (n & (n - 1)) == 0) {
+    while (cur.size() > 1) {
+      std::vector<Node> nxt;
+      for (size_t i = 0; i + 1 < cur.size(); i += 2) nxt.push_back(node_combine_h(cur[i], cur[i + 1]));
+      cur.swap(nxt);
+    }
+    return cur[0];
+  }
+  Node acc = cur[0];
+  for (size_t i = 1; i < n; ++i) acc = node_combine_h(acc, cur[i]);
+  return acc;
+}
+
+static void check_f64_args(const double* a, int n, int algo) {
+  PK_REQUIRE(a != nullptr, kErrArg, "null matrix pointer");
+  PK_REQUIRE(n >= 1, kErrArg, "empty matrix");
+  PK_REQUIRE(algo == 0 || algo == 1, kErrArg, "algo must be 0 (ryser) or 1 (glynn)");
+  PK_REQUIRE(n <= kBlockMaxN, kErrLimit, "dimension exceeds 64");
+}
+
+static void check_range(int m, uint64_t start, uint64_t length) {
+  const uint64_t total = m >= 64 ? ~0ull : (1ull << m);
+  PK_REQUIRE(start <= total && length <= total - start, kErrArg,
+             "Gray range [start, start+length) exceeds 2^m");
+}
+
+// ---------------------------------------------------------------------------
+// F_p host arithmetic
+
+using u128 = unsigned __int128;
+static uint64_t mulmod_h(uint64_t a, uint64_t b, uint64_t p) {
+  return static_cast<uint64_t>(static_cast<u128>(a) * b % p);
+}
+static uint64_t powmod_h(uint64_t b, uint64_t e, uint64_t p) {
+  uint64_t r = 1 % p;
+  b %= p;
+  while (e) {
+    if (e & 1) r = mulmod_h(r, b, p);
+    b = mulmod_h(b, b, p);
+    e >>= 1;
+  }
+  return r;
+}
+// 2^(bits * reps) mod p
+static uint64_t pow2mod_h(uint64_t bits_times_reps, uint64_t p) { return powmod_h(2, bits_times_reps, p); }
+
+static bool fast_prime(uint64_t p) { return (p & 1) && p >= 3 && p < (1ull << 31); }
+// exact integer row sums fit 31 bits: n (p - 1) < 2^31
+static bool lazy_prime(uint64_t p, int n) {
+  return fast_prime(p) && static_cast<uint64_t>(n) * (p - 1) < (1ull << 31);
+}
+
+}  // namespace pk
+
+// ===========================================================================
+// extern "C"
+
+using namespace pk;
+
+extern "C" const char* pk_last_error(void) { return last_error_cstr(); }
+
+extern "C" int pk_version(void) { return 100; }
+
+extern "C" int pk_max_n(void) { return kMaxN; }
+
+extern "C" int pk_device_count(void) {
+  return pk_guard([&]() -> int { return device_count(); });
+}
+
+namespace pk {
+
+// fp64 range on ndev devices
+static Node f64_range(const double* a, int n, bool cplx, int algo, uint64_t start,
+                      uint64_t length, int ndev, bool want_abs) {
+  check_f64_args(a, n, algo);
+  const Plan p = make_plan(n, algo, 1);
+  check_range(p.m, start, length);
+  const Range r = make_range(p, start, length);
+  const size_t abytes = static_cast<size_t>(n) * n * (cplx ? 16 : 8);
+  const uint64_t nt = r.t1 - r.t0;
+  ndev = nt ? clamp_ndev(ndev) : 1;
+  // split tiles on group boundaries
+  std::vector<uint64_t> cut(ndev + 1);
+  for (int d = 0; d <= ndev; ++d) {
+    uint64_t t = r.t0 + nt * d / ndev;
+    if (d > 0 && d < ndev) t = std::max(r.t0, std::min(r.t1, (t + p.group / 2) / p.group * p.group));
+    cut[d] = t;
+  }
+  std::vector<Node> roots(ndev);
+  std::vector<char> has(ndev, 0);
+  std::vector<Node> head, tail;
+  for_devices(ndev, [&](int d) {
+    DevCtx& c = ctx(d);
+    std::lock_guard<std::mutex> g(c.mu);
+    PK_CUDA(cudaSetDevice(c.dev));
+    auto* d_a = static_cast<double*>(c.a.get(abytes));
+    PK_CUDA(cudaMemcpyAsync(d_a, a, abytes, cudaMemcpyHostToDevice, c.stream));
+    const uint64_t t0 = cut[d], t1 = cut[d + 1];
+    if (t1 > t0) {
+      auto* d_part = static_cast<double*>(c.partials.get((t1 - t0) * kPartialStride * 8));
+      auto* d_out = static_cast<double*>(c.out.get(kPartialStride * 8));
+      F64Launch L = prepare_f64(c, p, cplx, algo, 1, d_a, t0, t1 - t0, want_abs, d_part);
+      launch_walk(c, L.fn, L.grid, L.smem, L.args);
+      launch_reduce(c, d_part, 1, t0, t1 - t0, p.group, d_out);
+      double h[kPartialStride];
+      PK_CUDA(cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+      PK_CUDA(cudaStreamSynchronize(c.stream));
+      roots[d] = node_from5(h);
+      has[d] = 1;
+    }
+    if (d == 0) {
+      head = run_f64_pieces(c, d_a, n, cplx, algo, r.head, want_abs);
+      tail = run_f64_pieces(c, d_a, n, cplx, algo, r.tail, want_abs);
+    }
+  });
+  std::vector<Node> rr;
+  for (int d = 0; d < ndev; ++d)
+    if (has[d]) rr.push_back(roots[d]);
+  std::vector<Node> seq = head;
+  if (!rr.empty()) seq.push_back(combine_roots(rr));
+  seq.insert(seq.end(), tail.begin(), tail.end());
+  if (seq.empty()) return Node{};
+  Node acc = seq[0];
+  for (size_t i = 1; i < seq.size(); ++i) acc = node_combine_h(acc, seq[i]);
+  return acc;
+}
+
+}  // namespace pk
+
+extern "C" int pk_ryser_f64(const double* a, int n, int is_complex, int algo, uint64_t start,
+                            uint64_t length, int ndev, double out[4], double* abs_sum) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(out != nullptr, kErrArg, "null output pointer");
+    const Node v = f64_range(a, n, is_complex != 0, algo, start, length, ndev, abs_sum != nullptr);
+    out[0] = v.re.s;
+    out[1] = v.im.s;
+    out[2] = v.re.c;
+    out[3] = v.im.c;
+    if (abs_sum) *abs_sum = v.ab;
+    return 0;
+  });
+}
+
+extern "C" int pk_ryser_f64_blocks(const double* a, int n, int is_complex, int algo,
+                                   const uint64_t* starts, const uint64_t* lens, int nblocks,
+                                   int device, double* out) {
+  return pk_guard([&]() -> int {
+    check_f64_args(a, n, algo);
+    PK_REQUIRE(nblocks >= 0, kErrArg, "negative block count");
+    if (nblocks == 0) return 0;
+    PK_REQUIRE(starts && lens && out, kErrArg, "null block arrays");
+    const int m = algo == 0 ? n : n - 1;
+    for (int i = 0; i < nblocks; ++i) check_range(m, starts[i], lens[i]);
+    DevCtx& c = ctx(device);
+    std::lock_guard<std::mutex> g(c.mu);
+    PK_CUDA(cudaSetDevice(c.dev));
+    const size_t abytes = static_cast<size_t>(n) * n * (is_complex ? 16 : 8);
+    auto* d_a = static_cast<double*>(c.a.get(abytes));
+    PK_CUDA(cudaMemcpyAsync(d_a, a, abytes, cudaMemcpyHostToDevice, c.stream));
+    std::vector<std::pair<uint64_t, uint64_t>> pcs(nblocks);
+    for (int i = 0; i < nblocks; ++i) pcs[i] = {starts[i], lens[i]};
+    const std::vector<Node> v = run_f64_pieces(c, d_a, n, is_complex != 0, algo, pcs, false);
+    for (int i = 0; i < nblocks; ++i) {
+      out[4 * i + 0] = v[i].re.s;
+      out[4 * i + 1] = v[i].im.s;
+      out[4 * i + 2] = v[i].re.c;
+      out[4 * i + 3] = v[i].im.c;
+    }
+    return 0;
+  });
+}
+
+extern "C" int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex, int algo,
+                                  int ndev, double* out, double* abs_sums) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(B >= 0, kErrArg, "negative batch size");
+    if (B == 0) return 0;
+    check_f64_args(a, n, algo);
+    PK_REQUIRE(out != nullptr, kErrArg, "null output pointer");
+    const bool cplx = is_complex != 0;
+    const size_t mat = static_cast<size_t>(n) * n * (cplx ? 2 : 1);
+    ndev = clamp_ndev(ndev);
+    ndev = std::min(ndev, B);
+    for_devices(ndev, [&](int d) {
+      const int b0 = static_cast<int>(static_cast<int64_t>(B) * d / ndev);
+      const int b1 = static_cast<int>(static_cast<int64_t>(B) * (d + 1) / ndev);
+      const int nb = b1 - b0;
+      if (nb <= 0) return;
+      DevCtx& c = ctx(d);
+      std::lock_guard<std::mutex> g(c.mu);
+      PK_CUDA(cudaSetDevice(c.dev));
+      const Plan p = make_plan(n, algo, nb);
+      auto* d_a = static_cast<double*>(c.a.get(nb * mat * 8));
+      PK_CUDA(cudaMemcpyAsync(d_a, a + b0 * mat, nb * mat * 8, cudaMemcpyHostToDevice, c.stream));
+      std::vector<double> h(static_cast<size_t>(nb) * kPartialStride);
+      if (p.k > 0) {
+        const uint64_t nt = p.tiles_total;
+        auto* d_part = static_cast<double*>(c.partials.get(nb * nt * kPartialStride * 8));
+        auto* d_out = static_cast<double*>(c.out.get(nb * kPartialStride * 8));
+        F64Launch L = prepare_f64(c, p, cplx, algo, nb, d_a, 0, nt, abs_sums != nullptr, d_part);
+        launch_walk(c, L.fn, L.grid, L.smem, L.args);
+        launch_reduce(c, d_part, nb, 0, nt, p.group, d_out);
+        PK_CUDA(cudaMemcpyAsync(h.data(), d_out, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+        PK_CUDA(cudaStreamSynchronize(c.stream));
+      } else {
+        // tiny m: one exact piece per matrix (2^m <= 32 terms)
+        for (int b = 0; b < nb; ++b) {
+          std::vector<std::pair<uint64_t, uint64_t>> pc{{0, 1ull << p.m}};
+          const std::vector<Node> v =
+              run_f64_pieces(c, d_a + b * mat, n, cplx, algo, pc, abs_sums != nullptr);
+          const Node& x = v[0];
+          double* o = h.data() + b * kPartialStride;
+          o[0] = x.re.s;
+          o[1] = x.re.c;
+          o[2] = x.im.s;
+          o[3] = x.im.c;
+          o[4] = x.ab;
+        }
+      }
+      for (int b = 0; b < nb; ++b) {
+        const double* o = h.data() + b * kPartialStride;
+        double* r = out + 4 * static_cast<size_t>(b0 + b);
+        r[0] = o[0];
+        r[1] = o[2];
+        r[2] = o[1];
+        r[3] = o[3];
+        if (abs_sums) abs_sums[b0 + b] = o[4];
+      }
+    });
+    return 0;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// F_p
+
+namespace pk {
+
+struct ModpGroup {
+  int P;                       // primes in the launch group (<= kMaxP)
+  bool lazy;                   // unreduced row sums (n p < 2^31) or reduced [0, p)
+  std::vector<int> idx;        // indices into the caller's prime list
+};
+
+// raw -> exact residue of the fast kernel: raw * sgn0 * 2^(32 (n-1)) mod p
+static uint64_t fix_fast(uint64_t raw, uint64_t p, int n, int algo) {
+  uint64_t v = mulmod_h(raw % p, pow2mod_h(32ull * (n - 1), p), p);
+  if (algo == 0 && (n & 1)) v = v == 0 ? 0 : p - v;
+  return v;
+}
+static uint64_t fix_block(uint64_t raw, uint64_t p, int n) {
+  if (!(p & 1)) return raw % p;
+  return mulmod_h(raw % p, pow2mod_h(64ull * (n - 1), p), p);
+}
+
+// generic walker for one modulus over pieces; returns the residue sum
+static uint64_t modp_pieces(DevCtx& c, const uint64_t* d_a, int n, int algo, uint64_t p,
+                            const std::vector<std::pair<uint64_t, uint64_t>>& pieces) {
+  if (pieces.empty()) return 0;
+  const int np = static_cast<int>(pieces.size());
+  std::vector<uint64_t> hs(np), hl(np), ho(np);
+  for (int i = 0; i < np; ++i) {
+    hs[i] = pieces[i].first;
+    hl[i] = pieces[i].second;
+  }
+  auto* ds = static_cast<uint64_t*>(c.starts.get(np * 8));
+  auto* dl = static_cast<uint64_t*>(c.lens.get(np * 8));
+  auto* dout = static_cast<uint64_t*>(c.blockout.get(np * 8));
+  PK_CUDA(cudaMemcpyAsync(ds, hs.data(), np * 8, cudaMemcpyHostToDevice, c.stream));
+  PK_CUDA(cudaMemcpyAsync(dl, hl.data(), np * 8, cudaMemcpyHostToDevice, c.stream));
+  const int grid = (np + kBlockThreads - 1) / kBlockThreads;
+  if (algo == 0)
+    block_modp_kernel<0><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, p, ds, dl, np, dout);
+  else
+    block_modp_kernel<1><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, p, ds, dl, np, dout);
+  PK_CUDA(cudaGetLastError());
+  PK_CUDA(cudaMemcpyAsync(ho.data(), dout, np * 8, cudaMemcpyDeviceToHost, c.stream));
+  PK_CUDA(cudaStreamSynchronize(c.stream));
+  uint64_t s = 0;
+  for (int i = 0; i < np; ++i) s = static_cast<uint64_t>((static_cast<u128>(s) + ho[i]) % p);
+  return fix_block(s, p, n);
+}
+
+struct ModpLaunch {
+  const void* fn;
+  int grid, smem, occ;
+  WalkArgs args;
+};
+
+static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, int P, bool lazy, int algo, int B,
+                               const uint32_t* d_a, const uint32_t* d_primes, uint64_t t0,
+                               uint64_t nt, unsigned long long* d_out) {
+  PK_REQUIRE(p.n >= 1 && p.n <= kMaxN, kErrLimit,
+             "dimension " + std::to_string(p.n) + " exceeds the GPU kernel range n <= " +
+                 std::to_string(kMaxN));
+  ModpLaunch L{};
+  L.fn = tables().modp[lazy ? 1 : 0][P][p.n];
+  PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing F_p kernel instantiation");
+  const int NP = (p.n + 3) & ~3;
+  const int per_warp = B > 1 ? 1 : 0;
+  L.smem = (2 * p.m + 1) * P * NP * 4 * (per_warp ? kWalkWarps : 1);
+  L.occ = occupancy(c, L.fn, kWalkThreads, L.smem);
+  const uint64_t units = static_cast<uint64_t>(B) * nt;
+  const uint64_t ctas = (units + kWalkWarps - 1) / kWalkWarps;
+  L.grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(c.sms) * L.occ));
+  WalkArgs& a = L.args;
+  a.a = d_a;
+  a.B = B;
+  a.n = p.n;
+  a.m = p.m;
+  a.algo = algo;
+  a.k = p.k;
+  a.per_warp_slot = per_warp;
+  a.tile0 = t0;
+  a.tiles = nt;
+  a.segs_total = 1ull << (p.m - p.k);
+  a.partials = nullptr;
+  a.modp_out = d_out;
+  a.primes = d_primes;
+  a.want_abs = 0;
+  return L;
+}
+
+static std::vector<ModpGroup> group_primes(const std::vector<int>& fast, const uint64_t* primes,
+                                           int n) {
+  std::vector<ModpGroup> gs;
+  for (int mode = 1; mode >= 0; --mode) {
+    std::vector<int> sel;
+    for (int k : fast)
+      if (lazy_prime(primes[k], n) == (mode == 1)) sel.push_back(k);
+    size_t i = 0;
+    while (i < sel.size()) {
+      const int P = static_cast<int>(std::min<size_t>(kMaxP, sel.size() - i));
+      ModpGroup g{P, mode == 1, {}};
+      for (int q = 0; q < P; ++q) g.idx.push_back(sel[i + q]);
+      gs.push_back(g);
+      i += P;
+    }
+  }
+  return gs;
+}
+
+// Upload the launch groups that share one P as a batch of B "matrices".
+static void pack_groups(const uint64_t* a, const uint64_t* primes, int n,
+                        const std::vector<ModpGroup>& gs, int P, bool lazy,
+                        std::vector<uint32_t>& ha, std::vector<uint32_t>& hp,
+                        std::vector<int>& which) {
+  const size_t nn = static_cast<size_t>(n) * n;
+  for (size_t gi = 0; gi < gs.size(); ++gi) {
+    if (gs[gi].P != P || gs[gi].lazy != lazy) continue;
+    which.push_back(static_cast<int>(gi));
+    for (int q = 0; q < P; ++q) {
+      const int k = gs[gi].idx[q];
+      hp.push_back(static_cast<uint32_t>(primes[k]));
+      for (size_t e = 0; e < nn; ++e) ha.push_back(static_cast<uint32_t>(a[k * nn + e]));
+    }
+  }
+}
+
+}  // namespace pk
+
+extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, int n, int algo,
+                             uint64_t start, uint64_t length, int ndev, uint64_t* out) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(P >= 0, kErrArg, "negative prime count");
+    if (P == 0) return 0;
+    PK_REQUIRE(a && primes && out, kErrArg, "null pointer argument");
+    PK_REQUIRE(n >= 1, kErrArg, "empty matrix");
+    PK_REQUIRE(algo == 0 || algo == 1, kErrArg, "algo must be 0 (ryser) or 1 (glynn)");
+    PK_REQUIRE(n <= kBlockMaxN, kErrLimit, "dimension exceeds 64");
+    const size_t nn = static_cast<size_t>(n) * n;
+    for (int k = 0; k < P; ++k) {
+      PK_REQUIRE(primes[k] >= 2 && primes[k] < (1ull << 62), kErrArg,
+                 "modulus must be a prime in [2, 2^62)");
+      for (size_t e = 0; e < nn; ++e)
+        PK_REQUIRE(a[k * nn + e] < primes[k], kErrArg, "matrix residues must lie in [0, p)");
+    }
+    const Plan p = make_plan(n, algo, 1);
+    check_range(p.m, start, length);
+    const Range r = make_range(p, start, length);
+    const uint64_t nt = r.t1 - r.t0;
+    std::vector<int> fast, slow;
+    for (int k = 0; k < P; ++k) {
+      if (fast_prime(primes[k]) && n <= kMaxN && nt > 0)
+        fast.push_back(k);
+      else
+        slow.push_back(k);
+    }
+    std::vector<uint64_t> res(P, 0);
+    const std::vector<ModpGroup> gs = group_primes(fast, primes, n);
+    ndev = (nt && !gs.empty()) ? clamp_ndev(ndev) : 1;
+    std::vector<uint64_t> cut(ndev + 1);
+    for (int d = 0; d <= ndev; ++d) cut[d] = r.t0 + nt * d / ndev;
+    std::vector<std::vector<uint64_t>> dev_res(ndev, std::vector<uint64_t>(P, 0));
+    for_devices(ndev, [&](int d) {
+      DevCtx& c = ctx(d);
+      std::lock_guard<std::mutex> g(c.mu);
+      PK_CUDA(cudaSetDevice(c.dev));
+      const uint64_t t0 = cut[d], t1 = cut[d + 1];
+      // fast kernel over the aligned interior, one launch per distinct (mode, P)
+      for (int lz = 1; lz >= 0; --lz)
+      for (int PP = kMaxP; PP >= 1 && t1 > t0; --PP) {
+        std::vector<uint32_t> ha, hp;
+        std::vector<int> which;
+        pack_groups(a, primes, n, gs, PP, lz == 1, ha, hp, which);
+        if (which.empty()) continue;
+        const int B = static_cast<int>(which.size());
+        auto* d_a = static_cast<uint32_t*>(c.a.get(ha.size() * 4));
+        auto* d_p = static_cast<uint32_t*>(c.primes.get(hp.size() * 4));
+        auto* d_o = static_cast<unsigned long long*>(c.modp_out.get(hp.size() * 8));
+        PK_CUDA(cudaMemcpyAsync(d_a, ha.data(), ha.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        PK_CUDA(cudaMemcpyAsync(d_p, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        PK_CUDA(cudaMemsetAsync(d_o, 0, hp.size() * 8, c.stream));
+        ModpLaunch L = prepare_modp(c, p, PP, lz == 1, algo, B, d_a, d_p, t0, t1 - t0, d_o);
+        launch_walk(c, L.fn, L.grid, L.smem, L.args);
+        std::vector<unsigned long long> ho(hp.size());
+        PK_CUDA(cudaMemcpyAsync(ho.data(), d_o, ho.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+        PK_CUDA(cudaStreamSynchronize(c.stream));
+        for (int bi = 0; bi < B; ++bi)
+          for (int q = 0; q < PP; ++q) {
+            const int k = gs[which[bi]].idx[q];
+            dev_res[d][k] = fix_fast(ho[bi * PP + q], primes[k], n, algo);
+          }
+      }
+      if (d == 0) {
+        // ragged head/tail of fast primes, and every slow modulus, on device 0
+        auto* d_a = static_cast<uint64_t*>(c.a.get(nn * 8));
+        for (int k = 0; k < P; ++k) {
+          const bool is_fast = std::find(fast.begin(), fast.end(), k) != fast.end();
+          std::vector<std::pair<uint64_t, uint64_t>> pcs;
+          if (is_fast) {
+            pcs = r.head;
+            pcs.insert(pcs.end(), r.tail.begin(), r.tail.end());
+          } else {
+            const int bits = std::clamp(p.m - 17, 6, 62);
+            split_pieces(start, start + length, bits, pcs);
+          }
+          if (pcs.empty()) continue;
+          PK_CUDA(cudaMemcpyAsync(d_a, a + k * nn, nn * 8, cudaMemcpyHostToDevice, c.stream));
+          const uint64_t v = modp_pieces(c, d_a, n, algo, primes[k], pcs);
+          dev_res[0][k] = static_cast<uint64_t>((static_cast<u128>(dev_res[0][k]) + v) % primes[k]);
+        }
+      }
+    });
+    for (int k = 0; k < P; ++k) {
+      u128 s = 0;
+      for (int d = 0; d < ndev; ++d) s += dev_res[d][k];
+      out[k] = static_cast<uint64_t>(s % primes[k]);
+    }
+    return 0;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// resident jobs
+
+struct pk_job {
+  int kind = 0;  // 0 f64, 1 modp
+  DevCtx* c = nullptr;
+  Plan plan;
+  int algo = 0, n = 0, P = 0, B = 1;
+  bool cplx = false;
+  uint64_t t0 = 0, nt = 0;
+  void* d_a = nullptr;
+  double* d_part = nullptr;
+  double* d_out = nullptr;
+  uint32_t* d_primes = nullptr;
+  unsigned long long* d_modp = nullptr;
+  void* d_flush = nullptr;
+  size_t flush_cap = 0;
+  std::vector<uint64_t> primes;
+  std::vector<int> prime_order;  // caller index for each packed slot
+  const void* fn = nullptr;
+  int grid = 0, smem = 0, occ = 0;
+  WalkArgs args{};
+};
+
+static void job_free(pk_job* j) {
+  if (!j) return;
+  if (j->c) cudaSetDevice(j->c->dev);
+  cudaFree(j->d_a);
+  cudaFree(j->d_part);
+  cudaFree(j->d_out);
+  cudaFree(j->d_primes);
+  cudaFree(j->d_modp);
+  cudaFree(j->d_flush);
+  delete j;
+}
+
+extern "C" int pk_job_f64_create(int device, const double* a, int n, int is_complex, int algo,
+                                 uint64_t start, uint64_t length, pk_job** job) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(job != nullptr, kErrArg, "null job pointer");
+    check_f64_args(a, n, algo);
+    std::unique_ptr<pk_job, void (*)(pk_job*)> j(new pk_job, job_free);
+    j->kind = 0;
+    j->c = &ctx(device);
+    DevCtx& c = *j->c;
+    std::lock_guard<std::mutex> g(c.mu);
+    PK_CUDA(cudaSetDevice(c.dev));
+    j->plan = make_plan(n, algo, 1);
+    check_range(j->plan.m, start, length);
+    const Range r = make_range(j->plan, start, length);
+    PK_REQUIRE(r.head.empty() && r.tail.empty() && r.t1 > r.t0, kErrArg,
+               "job range must be aligned to the tile span 2^(k+5)");
+    j->algo = algo;
+    j->n = n;
+    j->cplx = is_complex != 0;
+    j->t0 = r.t0;
+    j->nt = r.t1 - r.t0;
+    const size_t abytes = static_cast<size_t>(n) * n * (j->cplx ? 16 : 8);
+    PK_CUDA(cudaMalloc(&j->d_a, abytes));
+    PK_CUDA(cudaMemcpy(j->d_a, a, abytes, cudaMemcpyHostToDevice));
+    PK_CUDA(cudaMalloc(&j->d_part, j->nt * kPartialStride * 8));
+    PK_CUDA(cudaMalloc(&j->d_out, kPartialStride * 8));
+    F64Launch L = prepare_f64(c, j->plan, j->cplx, algo, 1, static_cast<double*>(j->d_a), j->t0,
+                              j->nt, false, j->d_part);
+    j->fn = L.fn;
+    j->grid = L.grid;
+    j->smem = L.smem;
+    j->occ = L.occ;
+    j->args = L.args;
+    *job = j.release();
+    return 0;
+  });
+}
+
+extern "C" int pk_job_modp_create(int device, const uint64_t* a, const uint64_t* primes, int P,
+                                  int n, int algo, uint64_t start, uint64_t length, pk_job** job) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(job != nullptr && a && primes, kErrArg, "null pointer argument");
+    PK_REQUIRE(P >= 1, kErrArg, "need at least one prime");
+    PK_REQUIRE(n >= 1 && n <= kMaxN, kErrLimit, "dimension outside the GPU kernel range");
+    std::unique_ptr<pk_job, void (*)(pk_job*)> j(new pk_job, job_free);
+    j->kind = 1;
+    j->c = &ctx(device);
+    DevCtx& c = *j->c;
+    std::lock_guard<std::mutex> g(c.mu);
+    PK_CUDA(cudaSetDevice(c.dev));
+    std::vector<int> fast;
+    for (int k = 0; k < P; ++k) {
+      PK_REQUIRE(fast_prime(primes[k]), kErrArg, "resident F_p jobs need odd primes < 2^31");
+      fast.push_back(k);
+    }
+    const std::vector<ModpGroup> gs = group_primes(fast, primes, n);
+    for (const auto& gg : gs)
+      PK_REQUIRE(gg.P == gs.front().P && gg.lazy == gs.front().lazy, kErrArg,
+                 "resident F_p jobs need primes of one mode and a count that is a multiple "
+                 "of 4 or at most 4");
+    j->plan = make_plan(n, algo, 1);
+    check_range(j->plan.m, start, length);
+    const Range r = make_range(j->plan, start, length);
+    PK_REQUIRE(r.head.empty() && r.tail.empty() && r.t1 > r.t0, kErrArg,
+               "job range must be aligned to the tile span 2^(k+5)");
+    j->algo = algo;
+    j->n = n;
+    j->P = gs.front().P;
+    j->B = static_cast<int>(gs.size());
+    j->t0 = r.t0;
+    j->nt = r.t1 - r.t0;
+    std::vector<uint32_t> ha, hp;
+    std::vector<int> which;
+    pack_groups(a, primes, n, gs, j->P, gs.front().lazy, ha, hp, which);
+    for (int w : which)
+      for (int k : gs[w].idx) {
+        j->prime_order.push_back(k);
+        j->primes.push_back(primes[k]);
+      }
+    PK_CUDA(cudaMalloc(&j->d_a, ha.size() * 4));
+    PK_CUDA(cudaMemcpy(j->d_a, ha.data(), ha.size() * 4, cudaMemcpyHostToDevice));
+    PK_CUDA(cudaMalloc(&j->d_primes, hp.size() * 4));
+    PK_CUDA(cudaMemcpy(j->d_primes, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice));
+    PK_CUDA(cudaMalloc(&j->d_modp, hp.size() * 8));
+    ModpLaunch L = prepare_modp(c, j->plan, j->P, gs.front().lazy, algo, j->B,
+                                static_cast<uint32_t*>(j->d_a),
+                                j->d_primes, j->t0, j->nt, j->d_modp);
+    j->fn = L.fn;
+    j->grid = L.grid;
+    j->smem = L.smem;
+    j->occ = L.occ;
+    j->args = L.args;
+    *job = j.release();
+    return 0;
+  });
+}
+
+extern "C" int pk_job_run(pk_job* j, int iters, size_t flush_bytes, double* total_ms,
+                          double* walk_ms, double* out_f64, uint64_t* out_res) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(j != nullptr && iters >= 1, kErrArg, "bad job or iteration count");
+    DevCtx& c = *j->c;
+    std::lock_guard<std::mutex> g(c.mu);
+    PK_CUDA(cudaSetDevice(c.dev));
+    if (flush_bytes > j->flush_cap) {
+      if (j->d_flush) PK_CUDA(cudaFree(j->d_flush));
+      j->d_flush = nullptr;
+      PK_CUDA(cudaMalloc(&j->d_flush, flush_bytes));
+      j->flush_cap = flush_bytes;
+    }
+    std::vector<cudaEvent_t> ev(2 * iters + 2);
+    for (auto& e : ev) PK_CUDA(cudaEventCreate(&e));
+    const size_t nres = j->kind == 1 ? j->primes.size() : 0;
+    PK_CUDA(cudaEventRecord(ev[0], c.stream));
+    for (int it = 0; it < iters; ++it) {
+      if (flush_bytes) PK_CUDA(cudaMemsetAsync(j->d_flush, it & 0xff, flush_bytes, c.stream));
+      if (j->kind == 1) PK_CUDA(cudaMemsetAsync(j->d_modp, 0, nres * 8, c.stream));
+      PK_CUDA(cudaEventRecord(ev[2 + 2 * it], c.stream));
+      launch_walk(c, j->fn, j->grid, j->smem, j->args);
+      PK_CUDA(cudaEventRecord(ev[3 + 2 * it], c.stream));
+      if (j->kind == 0) launch_reduce(c, j->d_part, 1, j->t0, j->nt, j->plan.group, j->d_out);
+    }
+    PK_CUDA(cudaEventRecord(ev[1], c.stream));
+    PK_CUDA(cudaEventSynchronize(ev[1]));
+    float ms = 0;
+    PK_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    if (total_ms) *total_ms = ms;
+    double wsum = 0;
+    for (int it = 0; it < iters; ++it) {
+      PK_CUDA(cudaEventElapsedTime(&ms, ev[2 + 2 * it], ev[3 + 2 * it]));
+      wsum += ms;
+    }
+    if (walk_ms) *walk_ms = wsum;
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (j->kind == 0 && out_f64)
+      PK_CUDA(cudaMemcpy(out_f64, j->d_out, kPartialStride * 8, cudaMemcpyDeviceToHost));
+    if (j->kind == 1 && out_res) {
+      std::vector<unsigned long long> ho(nres);
+      PK_CUDA(cudaMemcpy(ho.data(), j->d_modp, nres * 8, cudaMemcpyDeviceToHost));
+      for (size_t s = 0; s < nres; ++s)
+        out_res[j->prime_order[s]] = fix_fast(ho[s], j->primes[s], j->n, j->algo);
+    }
+    return 0;
+  });
+}
+
+extern "C" int pk_job_info(pk_job* j, int64_t* info) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(j && info, kErrArg, "null argument");
+    cudaFuncAttributes fa{};
+    PK_CUDA(cudaSetDevice(j->c->dev));
+    PK_CUDA(cudaFuncGetAttributes(&fa, j->fn));
+    info[0] = j->plan.k;
+    info[1] = static_cast<int64_t>(j->nt);
+    info[2] = j->grid;
+    info[3] = j->occ;
+    info[4] = fa.numRegs;
+    info[5] = static_cast<int64_t>(fa.localSizeBytes);
+    info[6] = j->smem;
+    info[7] = j->kind == 0 ? 2 : 1;
+    return 0;
+  });
+}
+
+extern "C" void pk_job_destroy(pk_job* j) { job_free(j); }

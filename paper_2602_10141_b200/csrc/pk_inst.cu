@@ -1,0 +1,40 @@
+// Explicit instantiation of the templated walk kernels.
+//
+// Compiled several times by the Makefile with different -D settings so the
+// ~200 kernels build in parallel:
+//   -DPK_INST_F64 -DPK_CPLX=0|1 -DPK_N_LO=.. -DPK_N_HI=..      fp64 real/complex
+//   -DPK_INST_MODP -DPK_LAZY=0|1 -DPK_P=1..4 -DPK_N_LO=.. -DPK_N_HI=..  F_p, P primes per lane
+// Each object exports one registration function that stores the kernel
+// addresses for N in [PK_N_LO, PK_N_HI] into the dispatch tables (pk_capi.cu).
+#include <utility>
+
+#include "pk_registry.h"
+#include "pk_walk.cuh"
+
+#define PK_CAT2(a, b) a##b
+#define PK_CAT(a, b) PK_CAT2(a, b)
+
+namespace pk {
+
+#if defined(PK_INST_F64)
+template <int... I>
+static void fill(const void** tbl, std::integer_sequence<int, I...>) {
+  ((tbl[PK_N_LO + I] = reinterpret_cast<const void*>(&walk_f64_kernel<PK_N_LO + I, (PK_CPLX != 0)>)),
+   ...);
+}
+void PK_CAT(PK_CAT(PK_CAT(register_f64_c, PK_CPLX), _), PK_N_LO)(const void** tbl) {
+  fill(tbl, std::make_integer_sequence<int, PK_N_HI - PK_N_LO + 1>{});
+}
+#elif defined(PK_INST_MODP)
+template <int... I>
+static void fill(const void** tbl, std::integer_sequence<int, I...>) {
+  ((tbl[PK_N_LO + I] = reinterpret_cast<const void*>(&walk_modp_kernel<PK_N_LO + I, PK_P, (PK_LAZY != 0)>)), ...);
+}
+void PK_CAT(PK_CAT(PK_CAT(PK_CAT(PK_CAT(register_modp_l, PK_LAZY), _p), PK_P), _), PK_N_LO)(const void** tbl) {
+  fill(tbl, std::make_integer_sequence<int, PK_N_HI - PK_N_LO + 1>{});
+}
+#else
+#error "define PK_INST_F64 or PK_INST_MODP"
+#endif
+
+}  // namespace pk

@@ -1,0 +1,77 @@
+"""The CPU oracle (oracle/ryser_oracle.c) pinned against the reference's golden vectors.
+
+Bit-exact: every golden value came from the reference's own numba kernels
+(kernels.py:33-344) via tools/make_golden.py.
+"""
+import numpy as np
+import pytest
+
+from conftest import bits_equal, dec_c, dec_matrix, load_golden
+from oracle import oracle
+
+
+@pytest.fixture(scope="module")
+def f64g():
+    return load_golden("f64_blocks.json")
+
+
+def test_oracle_f64_blocks_bit_exact(f64g):
+    assert f64g["backend"] == "numba"
+    n_checked = 0
+    for case in f64g["cases"]:
+        a = dec_matrix(case["matrix"])
+        for b in case["blocks"]:
+            s, c = oracle.block_partial(a, b["start"], b["len"], case["algorithm"])
+            assert bits_equal(s, dec_c(b["sum"])), (case["kind"], case["algorithm"], b)
+            assert bits_equal(c, dec_c(b["comp"])), (case["kind"], case["algorithm"], b)
+            n_checked += 1
+    assert n_checked >= 80
+
+
+def test_oracle_modp_blocks_exact():
+    g = load_golden("modp_blocks.json")
+    for case in g["cases"]:
+        n, p = case["n"], case["p"]
+        if "matrix" in case:
+            a = np.array(case["matrix"], dtype=np.uint64).reshape(n, n)
+        else:
+            g_ = case["root"]
+            pw = [pow(g_, k, p) for k in range(n)]
+            a = np.array([[pw[(j * k) % n] for k in range(n)] for j in range(n)], dtype=np.uint64)
+        for b in case["blocks"]:
+            if case["bits"] if "bits" in case else 0:
+                if case.get("bits") == 59 and b["len"] > 2000:
+                    continue
+            got = oracle.block_partial_modp(a, b["start"], b["len"], p, case["algorithm"])
+            assert got == b["res"], (n, p, case["algorithm"], b)
+
+
+def test_oracle_mulmod_against_bigint():
+    rng = np.random.default_rng(5)
+    for bits in (31, 59, 62):
+        p = (1 << bits) - 1 if bits != 62 else (1 << 61) - 1
+        for _ in range(2000):
+            a, b = int(rng.integers(0, p)), int(rng.integers(0, p))
+            assert oracle.mulmod(a, b, p) == a * b % p
+
+
+def test_oracle_engine_combine_matches_reference_kats():
+    kats = {k["tag"]: k for k in load_golden("engine_kats.json")["kats"]}
+    g = load_golden("engine_kats.json")
+    a = dec_matrix(g["ginibre14"])
+    for blocks in (1, 7, 64):
+        want = dec_c(kats[f"blocked_ginibre14_{blocks}"]["v"])
+        got = oracle.permanent(a, "ryser", blocks=blocks, threads=4)
+        assert bits_equal(got, want), blocks
+
+
+def test_oracle_schur_values():
+    g = load_golden("schur.json")
+    for row in g["rows"]:
+        if row["n"] > 15:
+            continue
+        n = row["n"]
+        for p, root, res in zip(row["primes"], row["roots"], row["residues"]):
+            pw = [pow(root, k, p) for k in range(n)]
+            a = [[pw[(j * k) % n] for k in range(n)] for j in range(n)]
+            assert oracle.permanent_modp(a, p, blocks=8) == res

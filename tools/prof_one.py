@@ -1,0 +1,23 @@
+"""Run one resident walk for profiling:  python tools/prof_one.py {f64c|f64r|modp|modpr} N [iters]"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_10141_b200 import _native as nat  # noqa: E402
+from tools.gpu_probe import primes_1modn, schur_res  # noqa: E402
+
+kind, n = sys.argv[1], int(sys.argv[2])
+iters = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+rng = np.random.default_rng(3)
+if kind.startswith("f64"):
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    a = q if kind == "f64c" else q.real.copy()
+    job = nat.Job.f64(a, "ryser", 0, 1 << n)
+else:
+    below = (1 << 31) // n if kind == "modp" else (1 << 31)
+    ps = primes_1modn(n, below, 4)
+    job = nat.Job.modp(np.stack([schur_res(n, p) for p in ps]), ps, "ryser", 0, 1 << n)
+tot, walk, res = job.run(iters)
+print(kind, n, job.info(), f"walk {walk / iters:.3f} ms", f"{iters * n * 2.0 ** n * (4 if 'modp' in kind else 1) / (walk / 1e3):.3e} upd/s")
