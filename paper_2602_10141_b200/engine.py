@@ -342,6 +342,9 @@ def perm_batch(mats, method: str = "ryser", devices: int | None = None,
     B, n = mats.shape[0], mats.shape[1]
     if n == 0:
         raise ValueError("empty matrix")
+    if method == "naive":
+        vals = np.array([perm_naive(m) for m in mats])
+        return (vals, None) if want_abs else vals
     _check_gray_dims(n)
     if method not in (RYSER, GLYNN):
         raise ValueError(f"unknown method {method!r}")
