@@ -251,6 +251,12 @@ def main():
     roof_peak = fp64_peak / 6.0
     per_gpu_upd = length * n
     achieved = args.steps * per_gpu_upd / (walk_ms_max / 1e3)
+    traffic = None
+    try:  # DRAM bytes per walk launch from the committed ncu capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            traffic = json.load(f).get(f"walk_f64_kernel<{n},true>")
+    except OSError:
+        pass
 
     out = {
         "metric": METRIC, "value": value, "unit": "row-updates/s", "n_gpus": world,
@@ -268,7 +274,8 @@ def main():
                 "d2h_bytes_per_step": 32},
         "gpu_launches": int(args.steps * info["launches"]),
         "roofline": {"bound": "fp64", "achieved": achieved / 1e9, "peak": roof_peak / 1e9,
-                     "unit": "Gupd/s", "frac": achieved / roof_peak, "traffic": None,
+                     "unit": "Gupd/s", "frac": achieved / roof_peak, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per walk launch (ncu)",
                      "peak_basis": "R = measured DFMA lane-ops/s / 6 FP64 instructions per "
                                    "complex row update (2 DFMA update + DMUL,DFMA,DMUL,DFMA "
                                    "product)",
@@ -282,10 +289,10 @@ def main():
 
     if rank == 0 and world == 1:
         cores = os.cpu_count() or 1
-        rate, dt = cpu_rate(a, n, cores, 22)
+        rate, dt = cpu_rate(a, n, cores, 24)
         out["cpu_baseline"] = {"value": rate, "unit": "row-updates/s", "cores": cores,
                                "kind": "port",
-                               "sample": f"{cores} host threads x one 2^22-index block of the "
+                               "sample": f"{cores} host threads x one 2^24-index block of the "
                                          f"n={n} walk (oracle/ryser_oracle.c), {dt:.2f} s wall"}
         if not args.no_secondary:
             out["secondary"] = secondary(args, nat, modular)

@@ -136,6 +136,11 @@ void pk_job_destroy(pk_job* job);
 int pk_measure_peaks(int device, double* out, int max_out);
 const char* pk_peak_names(void);
 
+/* Dependent-chain latencies in SM cycles for the ops named by
+ * pk_latency_names() (one warp, one chain).  Returns the count. */
+int pk_measure_latencies(int device, double* out, int max_out);
+const char* pk_latency_names(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,8 @@ def _bind(lib):
         "pk_job_destroy": (None, [_vp]),
         "pk_measure_peaks": (_int, [_int, _vp, _int]),
         "pk_peak_names": (ctypes.c_char_p, []),
+        "pk_measure_latencies": (_int, [_int, _vp, _int]),
+        "pk_latency_names": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -81,7 +83,7 @@ def exported_symbols():
         "pk_last_error", "pk_device_count", "pk_version", "pk_max_n", "pk_ryser_f64",
         "pk_ryser_f64_blocks", "pk_ryser_f64_batch", "pk_ryser_modp", "pk_job_f64_create",
         "pk_job_modp_create", "pk_job_run", "pk_job_info", "pk_job_destroy",
-        "pk_measure_peaks", "pk_peak_names",
+        "pk_measure_peaks", "pk_peak_names", "pk_measure_latencies", "pk_latency_names",
     ]
 
 
@@ -190,6 +192,15 @@ def measure_peaks(device: int = 0) -> dict:
     names = lib().pk_peak_names().decode().split(",")
     return {names[i]: {"ops_per_s": float(buf[3 * i]), "ops_per_clk_sm": float(buf[3 * i + 1]),
                        "sm_mhz": float(buf[3 * i + 2])} for i in range(k)}
+
+
+def measure_latencies(device: int = 0) -> dict:
+    buf = np.zeros(16, dtype=np.float64)
+    k = lib().pk_measure_latencies(int(device), _ptr(buf), 16)
+    if k < 0:
+        _check(k)
+    names = lib().pk_latency_names().decode().split(",")
+    return {names[i]: float(buf[i]) for i in range(k)}
 
 
 class Job:

@@ -94,7 +94,7 @@ struct DevCtx {
   int sms = 0;
   cudaStream_t stream = nullptr;
   std::mutex mu;
-  DBuf a, partials, out, primes, starts, lens, blockout, blockabs, modp_out;
+  DBuf a, partials, groups, out, primes, starts, lens, blockout, blockabs, modp_out;
   std::map<std::pair<const void*, int>, int> occ;  // (kernel, smem) -> CTAs per SM
 };
 
@@ -167,14 +167,15 @@ static Plan make_plan(int n, int algo, int B) {
     p.piece_bits = std::max(m, 1);
     return p;
   }
-  const int kmin = std::min(m - 5, 8);
+  // tiles of 2^kTileBits segments of 2^k indices; ~2^17 tiles per launch
+  const int kmin = std::min(m - kTileBits, 8);
   if (B <= 1) {
-    p.k = std::max(kmin, m - 22);
+    p.k = std::max(kmin, m - kTileBits - 17);
   } else {
-    const int t = std::clamp(ilog2_floor(double(1 << 17) / B), 0, m - 5 - kmin);
-    p.k = m - 5 - t;
+    const int t = std::clamp(ilog2_floor(double(1 << 17) / B), 0, m - kTileBits - kmin);
+    p.k = m - kTileBits - t;
   }
-  p.tiles_total = 1ull << (m - p.k - 5);
+  p.tiles_total = 1ull << (m - p.k - kTileBits);
   p.group = std::max<uint64_t>(1, p.tiles_total / kMaxGroups);
   p.piece_bits = std::min(p.k, 10);
   return p;
@@ -205,7 +206,7 @@ static Range make_range(const Plan& p, uint64_t start, uint64_t length) {
     split_pieces(r.start, r.end, p.piece_bits, r.head);
     return r;
   }
-  const int tb = p.k + 5;
+  const int tb = p.k + kTileBits;
   const uint64_t ts = 1ull << tb;
   const uint64_t A = (start + ts - 1) / ts * ts, Bt = r.end / ts * ts;
   if (A < Bt) {
@@ -250,7 +251,7 @@ static F64Launch prepare_f64(DevCtx& c, const Plan& p, bool cplx, int algo, int 
   PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing fp64 kernel instantiation");
   L.per_warp = B > 1 ? 1 : 0;
   const int elem = cplx ? 16 : 8;
-  const int slot = (p.n + p.n * p.m) * elem;
+  const int slot = (p.m + 1) * col_stride(p.n, elem) * elem;
   L.smem = slot * (L.per_warp ? kWalkWarps : 1);
   L.occ = occupancy(c, L.fn, kWalkThreads, L.smem);
   const uint64_t units = static_cast<uint64_t>(B) * nt;
@@ -279,13 +280,23 @@ static void launch_walk(DevCtx& c, const void* fn, int grid, int smem, WalkArgs&
   PK_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kWalkThreads), kargs, smem, c.stream));
 }
 
+// Two-stage deterministic reduction of [B][nt] tile partials into [B][5]
+// roots; `groups` is scratch of >= B * (nt / group + 2) * 5 doubles.
 static void launch_reduce(DevCtx& c, const double* d_partials, int B, uint64_t t0, uint64_t nt,
-                          uint64_t group, double* d_out) {
+                          uint64_t group, double* d_groups, double* d_out) {
   const uint64_t g0 = t0 / group, g1 = (t0 + nt - 1) / group + 1;
+  const int ng = static_cast<int>(g1 - g0);
   PK_REQUIRE(g1 - g0 <= static_cast<uint64_t>(kMaxGroups) + 1, kErrInternal,
              "too many reduction groups");
-  reduce_tiles_kernel<<<B, kReduceThreads, 0, c.stream>>>(d_partials, t0, nt, group, d_out);
+  dim3 fg((ng + kFoldThreads - 1) / kFoldThreads, B);
+  fold_groups_kernel<<<fg, kFoldThreads, 0, c.stream>>>(d_partials, t0, nt, group, g0, ng, d_groups);
   PK_CUDA(cudaGetLastError());
+  tree_groups_kernel<<<B, kTreeThreads, 0, c.stream>>>(d_groups, g0, ng, d_out);
+  PK_CUDA(cudaGetLastError());
+}
+
+static size_t group_scratch_doubles(int B, uint64_t nt, uint64_t group) {
+  return static_cast<size_t>(B) * (nt / group + 2) * kPartialStride;
 }
 
 // exact-arithmetic pieces on one device; returns one Node per piece
@@ -471,7 +482,8 @@ static Node f64_range(const double* a, int n, bool cplx, int algo, uint64_t star
       auto* d_out = static_cast<double*>(c.out.get(kPartialStride * 8));
       F64Launch L = prepare_f64(c, p, cplx, algo, 1, d_a, t0, t1 - t0, want_abs, d_part);
       launch_walk(c, L.fn, L.grid, L.smem, L.args);
-      launch_reduce(c, d_part, 1, t0, t1 - t0, p.group, d_out);
+      auto* d_grp = static_cast<double*>(c.groups.get(group_scratch_doubles(1, t1 - t0, p.group) * 8));
+      launch_reduce(c, d_part, 1, t0, t1 - t0, p.group, d_grp, d_out);
       double h[kPartialStride];
       PK_CUDA(cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
       PK_CUDA(cudaStreamSynchronize(c.stream));
@@ -569,7 +581,8 @@ extern "C" int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex,
         auto* d_out = static_cast<double*>(c.out.get(nb * kPartialStride * 8));
         F64Launch L = prepare_f64(c, p, cplx, algo, nb, d_a, 0, nt, abs_sums != nullptr, d_part);
         launch_walk(c, L.fn, L.grid, L.smem, L.args);
-        launch_reduce(c, d_part, nb, 0, nt, p.group, d_out);
+        auto* d_grp = static_cast<double*>(c.groups.get(group_scratch_doubles(nb, nt, p.group) * 8));
+        launch_reduce(c, d_part, nb, 0, nt, p.group, d_grp, d_out);
         PK_CUDA(cudaMemcpyAsync(h.data(), d_out, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
         PK_CUDA(cudaStreamSynchronize(c.stream));
       } else {
@@ -666,9 +679,8 @@ static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, int P, bool lazy, int a
   ModpLaunch L{};
   L.fn = tables().modp[lazy ? 1 : 0][P][p.n];
   PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing F_p kernel instantiation");
-  const int NP = (p.n + 3) & ~3;
   const int per_warp = B > 1 ? 1 : 0;
-  L.smem = (2 * p.m + 1) * P * NP * 4 * (per_warp ? kWalkWarps : 1);
+  L.smem = (2 * p.m + 1) * P * col_stride(p.n, 4) * 4 * (per_warp ? kWalkWarps : 1);
   L.occ = occupancy(c, L.fn, kWalkThreads, L.smem);
   const uint64_t units = static_cast<uint64_t>(B) * nt;
   const uint64_t ctas = (units + kWalkWarps - 1) / kWalkWarps;
@@ -691,16 +703,21 @@ static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, int P, bool lazy, int a
   return L;
 }
 
+// Primes per lane: four while the register-resident state (P x n words) fits
+// without spilling, three for n > 36.
+static int max_primes_per_lane(int n) { return n <= 36 ? kMaxP : 3; }
+
 static std::vector<ModpGroup> group_primes(const std::vector<int>& fast, const uint64_t* primes,
                                            int n) {
   std::vector<ModpGroup> gs;
+  const int pmax = max_primes_per_lane(n);
   for (int mode = 1; mode >= 0; --mode) {
     std::vector<int> sel;
     for (int k : fast)
       if (lazy_prime(primes[k], n) == (mode == 1)) sel.push_back(k);
     size_t i = 0;
     while (i < sel.size()) {
-      const int P = static_cast<int>(std::min<size_t>(kMaxP, sel.size() - i));
+      const int P = static_cast<int>(std::min<size_t>(pmax, sel.size() - i));
       ModpGroup g{P, mode == 1, {}};
       for (int q = 0; q < P; ++q) g.idx.push_back(sel[i + q]);
       gs.push_back(g);
@@ -833,6 +850,7 @@ struct pk_job {
   uint64_t t0 = 0, nt = 0;
   void* d_a = nullptr;
   double* d_part = nullptr;
+  double* d_groups = nullptr;
   double* d_out = nullptr;
   uint32_t* d_primes = nullptr;
   unsigned long long* d_modp = nullptr;
@@ -850,6 +868,7 @@ static void job_free(pk_job* j) {
   if (j->c) cudaSetDevice(j->c->dev);
   cudaFree(j->d_a);
   cudaFree(j->d_part);
+  cudaFree(j->d_groups);
   cudaFree(j->d_out);
   cudaFree(j->d_primes);
   cudaFree(j->d_modp);
@@ -883,6 +902,7 @@ extern "C" int pk_job_f64_create(int device, const double* a, int n, int is_comp
     PK_CUDA(cudaMemcpy(j->d_a, a, abytes, cudaMemcpyHostToDevice));
     PK_CUDA(cudaMalloc(&j->d_part, j->nt * kPartialStride * 8));
     PK_CUDA(cudaMalloc(&j->d_out, kPartialStride * 8));
+    PK_CUDA(cudaMalloc(&j->d_groups, group_scratch_doubles(1, j->nt, j->plan.group) * 8));
     F64Launch L = prepare_f64(c, j->plan, j->cplx, algo, 1, static_cast<double*>(j->d_a), j->t0,
                               j->nt, false, j->d_part);
     j->fn = L.fn;
@@ -977,7 +997,8 @@ extern "C" int pk_job_run(pk_job* j, int iters, size_t flush_bytes, double* tota
       PK_CUDA(cudaEventRecord(ev[2 + 2 * it], c.stream));
       launch_walk(c, j->fn, j->grid, j->smem, j->args);
       PK_CUDA(cudaEventRecord(ev[3 + 2 * it], c.stream));
-      if (j->kind == 0) launch_reduce(c, j->d_part, 1, j->t0, j->nt, j->plan.group, j->d_out);
+      if (j->kind == 0)
+        launch_reduce(c, j->d_part, 1, j->t0, j->nt, j->plan.group, j->d_groups, j->d_out);
     }
     PK_CUDA(cudaEventRecord(ev[1], c.stream));
     PK_CUDA(cudaEventSynchronize(ev[1]));
@@ -1016,7 +1037,7 @@ extern "C" int pk_job_info(pk_job* j, int64_t* info) {
     info[4] = fa.numRegs;
     info[5] = static_cast<int64_t>(fa.localSizeBytes);
     info[6] = j->smem;
-    info[7] = j->kind == 0 ? 2 : 1;
+    info[7] = j->kind == 0 ? 3 : 1;
     return 0;
   });
 }

@@ -186,6 +186,66 @@ int run_peak(int sms, int blocks_per_sm, int iters, double* ops_per_s, double* o
   return 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// Dependent-chain latencies (one warp per SM, one chain): cycles per op.
+template <int OP>
+__global__ void lat_kernel(int iters, uint64_t* sink, long long* cyc, uint64_t magic) {
+  __shared__ uint32_t sm[64];
+  const unsigned tid = threadIdx.x;
+  if (tid < 64) sm[tid] = (tid + 1) & 63;
+  __syncthreads();
+  uint64_t keep = 0;
+  long long t0 = clock64();
+  if constexpr (OP == 0) {  // DFMA
+    double x = 0.5 + tid;
+    for (int i = 0; i < iters; ++i) asm volatile("fma.rn.f64 %0, %0, %0, %0;" : "+d"(x));
+    keep = __double_as_longlong(x);
+  } else if constexpr (OP == 1) {  // DMUL -> DFMA pair (one complex-product link)
+    double x = 0.5 + tid, y = 0.25;
+    for (int i = 0; i < iters; ++i) {
+      asm volatile("mul.rn.f64 %0, %0, %1;" : "+d"(y) : "d"(x));
+      asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(x) : "d"(y));
+    }
+    keep = __double_as_longlong(x);
+  } else if constexpr (OP == 2) {  // IMAD
+    uint32_t x = tid + 3;
+    for (int i = 0; i < iters; ++i) asm volatile("mad.lo.u32 %0, %0, %0, %0;" : "+r"(x));
+    keep = x;
+  } else if constexpr (OP == 3) {  // Montgomery REDC link
+    uint32_t y = tid + 5;
+    const uint32_t p = 1073741789u, mneg = mont_neg_inv32(p);
+    for (int i = 0; i < iters; ++i) y = mont_lazy(y, y, p, mneg);
+    keep = y;
+  } else if constexpr (OP == 4) {  // LDS
+    uint32_t x = tid & 63;
+    for (int i = 0; i < iters; ++i) x = sm[x];
+    keep = x;
+  } else {  // SHFL
+    uint32_t x = tid;
+    for (int i = 0; i < iters; ++i) x = __shfl_xor_sync(0xffffffffu, x, 1) + 1;
+    keep = x;
+  }
+  long long t1 = clock64();
+  if (keep == magic) sink[tid] = keep;
+  if (tid == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int OP>
+double run_lat(int iters) {
+  uint64_t* sink = nullptr;
+  long long* cyc = nullptr;
+  PK_CUDA(cudaMalloc(&sink, sizeof(uint64_t) * 32));
+  PK_CUDA(cudaMalloc(&cyc, sizeof(long long)));
+  lat_kernel<OP><<<1, 32>>>(iters / 4, sink, cyc, 0x5eedull);
+  lat_kernel<OP><<<1, 32>>>(iters, sink, cyc, 0x5eedull);
+  PK_CUDA(cudaGetLastError());
+  long long h = 0;
+  PK_CUDA(cudaMemcpy(&h, cyc, sizeof(h), cudaMemcpyDeviceToHost));
+  cudaFree(sink);
+  cudaFree(cyc);
+  return double(h) / iters;
+}
 }  // namespace
 }  // namespace pk
 
@@ -222,4 +282,20 @@ extern "C" int pk_measure_peaks(int device, double* out, int max_out) {
 
 extern "C" const char* pk_peak_names(void) {
   return "dfma,dadd,dmul,imad,imad_wide,imad_hi,iadd3,mont_mul_3imad,ffma";
+}
+
+extern "C" int pk_measure_latencies(int device, double* out, int max_out) {
+  using namespace pk;
+  return pk_guard([&]() -> int {
+    PK_CUDA(cudaSetDevice(device));
+    const int iters = 1 << 14;
+    double v[6] = {run_lat<0>(iters), run_lat<1>(iters), run_lat<2>(iters),
+                   run_lat<3>(iters), run_lat<4>(iters), run_lat<5>(iters)};
+    for (int i = 0; i < 6 && i < max_out; ++i) out[i] = v[i];
+    return 6;
+  });
+}
+
+extern "C" const char* pk_latency_names(void) {
+  return "dfma,dmul_dfma_pair,imad,mont_redc,lds,shfl";
 }

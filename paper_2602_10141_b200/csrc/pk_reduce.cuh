@@ -2,7 +2,8 @@
 //
 // Tiles of one matrix are grouped by GLOBAL index into groups of c tiles
 // (c = max(1, tiles_total / kMaxGroups), a power of two fixed by n, never by
-// the device count).  A group is a left fold of pair_combine; groups are then
+// the device count).  Two launches: fold_groups_kernel (one thread per group,
+// many CTAs) and tree_groups_kernel (one CTA per matrix).  A group is a left fold of pair_combine; groups are then
 // combined by a binary tree whose nodes are also aligned on global indices.
 // A device that owns an aligned power-of-two run of groups therefore produces
 // exactly one subtree root, and combining the device roots with the same rule
@@ -19,8 +20,10 @@
 
 namespace pk {
 
-constexpr int kMaxGroups = 512;
-constexpr int kReduceThreads = 256;
+constexpr int kMaxGroups = 4096;   // groups per matrix and launch (see make_plan)
+constexpr int kFoldThreads = 128;
+constexpr int kTreeThreads = 512;
+constexpr int kRegLevels = 3;      // tree levels combined in registers (8 groups per thread)
 constexpr int kPartialStride = 5;  // s_re, c_re, s_im, c_im, abs
 
 struct Node5 {
@@ -32,32 +35,73 @@ __device__ __forceinline__ Node5 node_combine(const Node5& a, const Node5& b) {
   return Node5{pair_combine(a.re, b.re), pair_combine(a.im, b.im), a.ab + b.ab};
 }
 
-// partials: [B][tiles][5] for global tiles [tile0, tile0 + tiles); out: [B][5]
-__global__ void __launch_bounds__(kReduceThreads) reduce_tiles_kernel(const double* __restrict__ partials,
-                                                                      uint64_t tile0, uint64_t tiles,
-                                                                      uint64_t c, double* out) {
-  __shared__ Node5 buf[2][kMaxGroups + 2];
-  const int b = blockIdx.x;
+__device__ __forceinline__ Node5 load_node(const double* q) {
+  return Node5{Pair{q[0], q[1]}, Pair{q[2], q[3]}, q[4]};
+}
+
+__device__ __forceinline__ void store_node(double* q, const Node5& v) {
+  q[0] = v.re.s;
+  q[1] = v.re.c;
+  q[2] = v.im.s;
+  q[3] = v.im.c;
+  q[4] = v.ab;
+}
+
+// Stage 1: left fold of each group of c tiles (one thread per group).
+// partials: [B][tiles][5] for global tiles [tile0, tile0 + tiles);
+// groups:   [B][ng][5] for global groups [g0, g0 + ng).
+__global__ void __launch_bounds__(kFoldThreads) fold_groups_kernel(
+    const double* __restrict__ partials, uint64_t tile0, uint64_t tiles, uint64_t c, uint64_t g0,
+    int ng, double* __restrict__ groups) {
+  const int b = blockIdx.y;
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= ng) return;
   const double* P = partials + static_cast<uint64_t>(b) * tiles * kPartialStride;
-  const uint64_t g0 = tile0 / c, g1 = (tile0 + tiles - 1) / c + 1;
-  const int ng = static_cast<int>(g1 - g0);
-  for (int gi = threadIdx.x; gi < ng; gi += blockDim.x) {
-    const uint64_t lo = max((g0 + gi) * c, tile0), hi = min((g0 + gi + 1) * c, tile0 + tiles);
-    Node5 acc{};
-    bool first = true;
-    for (uint64_t t = lo; t < hi; ++t) {
-      const double* q = P + (t - tile0) * kPartialStride;
-      const Node5 v{Pair{q[0], q[1]}, Pair{q[2], q[3]}, q[4]};
-      acc = first ? v : node_combine(acc, v);
-      first = false;
+  const uint64_t lo = max((g0 + gi) * c, tile0), hi = min((g0 + gi + 1) * c, tile0 + tiles);
+  Node5 acc = load_node(P + (lo - tile0) * kPartialStride);
+#pragma unroll 4
+  for (uint64_t t = lo + 1; t < hi; ++t) acc = node_combine(acc, load_node(P + (t - tile0) * kPartialStride));
+  store_node(groups + (static_cast<uint64_t>(b) * ng + gi) * kPartialStride, acc);
+}
+
+// Stage 2: binary tree over the groups on GLOBAL indices (level L node j covers
+// groups [j 2^L, (j+1) 2^L)); missing children pass their sibling through.  The
+// first kRegLevels levels are combined in registers, the rest in shared memory.
+__global__ void __launch_bounds__(kTreeThreads) tree_groups_kernel(const double* __restrict__ groups,
+                                                                    uint64_t g0, int ng,
+                                                                    double* __restrict__ out) {
+  constexpr int kLeaves = 1 << kRegLevels;
+  __shared__ Node5 buf[2][kMaxGroups / kLeaves + 2];
+  const int b = blockIdx.x;
+  const double* G = groups + static_cast<uint64_t>(b) * ng * kPartialStride;
+  const uint64_t g1 = g0 + ng;  // exclusive
+  uint64_t lo_prev = g0 >> kRegLevels, hi_prev = (g1 - 1) >> kRegLevels;
+  const int cnt0 = static_cast<int>(hi_prev - lo_prev + 1);
+  for (int t = threadIdx.x; t < cnt0; t += blockDim.x) {
+    const uint64_t j = lo_prev + t;
+    Node5 v[kLeaves];
+    bool has[kLeaves];
+#pragma unroll
+    for (int e = 0; e < kLeaves; ++e) {
+      const uint64_t g = j * kLeaves + e;
+      has[e] = g >= g0 && g < g1;
+      if (has[e]) v[e] = load_node(G + (g - g0) * kPartialStride);
     }
-    buf[0][gi] = acc;
+#pragma unroll
+    for (int w = 1; w < kLeaves; w *= 2)
+#pragma unroll
+      for (int e = 0; e + w < kLeaves; e += 2 * w) {
+        if (has[e] && has[e + w])
+          v[e] = node_combine(v[e], v[e + w]);
+        else if (has[e + w])
+          v[e] = v[e + w];
+        has[e] = has[e] || has[e + w];
+      }
+    buf[0][t] = v[0];
   }
   __syncthreads();
-  // binary tree on global indices: level L node j covers groups [j 2^L, (j+1) 2^L)
   int cur = 0;
-  uint64_t lo_prev = g0, hi_prev = g1 - 1;  // inclusive node index range at level L-1
-  for (int L = 1; lo_prev != hi_prev; ++L) {
+  while (lo_prev != hi_prev) {
     const uint64_t lo = lo_prev >> 1, hi = hi_prev >> 1;
     const int cnt = static_cast<int>(hi - lo + 1);
     for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
@@ -78,15 +122,7 @@ __global__ void __launch_bounds__(kReduceThreads) reduce_tiles_kernel(const doub
     lo_prev = lo;
     hi_prev = hi;
   }
-  if (threadIdx.x == 0) {
-    const Node5 v = buf[cur][0];
-    double* o = out + static_cast<uint64_t>(b) * kPartialStride;
-    o[0] = v.re.s;
-    o[1] = v.re.c;
-    o[2] = v.im.s;
-    o[3] = v.im.c;
-    o[4] = v.ab;
-  }
+  if (threadIdx.x == 0) store_node(out + static_cast<uint64_t>(b) * kPartialStride, buf[cur][0]);
 }
 
 }  // namespace pk

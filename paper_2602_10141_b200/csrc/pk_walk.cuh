@@ -14,12 +14,16 @@
 //   segment = 2^k consecutive Gray indices walked by ONE lane; segments are
 //             aligned, so at step s of every lane the flip column is ctz(s)
 //             (warp-uniform => shared-memory broadcast, no divergence) and the
-//             flip direction is bit (ctz(s)+1) of s, except at ctz(s) = k-1
+//             flip direction is bit ctz(s)+1 of s, except at ctz(s) = k-1
 //             where it is bit 0 of the segment index (per lane).
-//   tile    = 32 consecutive segments = one warp; the warp reduces its 32
-//             lanes with a fixed shuffle tree -> one partial per tile.
+//   product = a balanced binary tree over the n state entries (n-1 multiplies,
+//             depth log2 n): the FP64 complex link (DMUL->DFMA) is 16 cycles
+//             and a Montgomery REDC link 28 cycles on B200, so a serial chain
+//             is latency bound at 2-3 resident warps per scheduler.
+//   tile    = 32 consecutive segments = one warp; the warp reduces its lanes
+//             with a fixed shuffle tree -> one partial per tile.
 //   Tiles are spread over a persistent grid (grid-stride over warps); tile
-//   partials are reduced by pk_reduce_tiles in a fixed, device-count
+//   partials are reduced by reduce_tiles_kernel in a fixed, device-count
 //   independent tree (fp64) or summed mod p (F_p, exact, order-free).
 // The start state of a segment is rebuilt in O((m-k) n) from gray(start),
 // mirroring gray.block_start_state (reference gray.py:88-114).
@@ -31,10 +35,14 @@
 
 #include "pk_common.cuh"
 
+#ifndef PK_MINCTA_T
+#define PK_MINCTA_T 64
+#endif
 namespace pk {
 
 constexpr int kWalkThreads = 128;  // 4 warps per CTA
 constexpr int kWalkWarps = kWalkThreads / 32;
+constexpr int kTileBits = 5;       // 32 segments (lanes) per warp-tile
 
 struct WalkArgs {
   const void* a;         // B matrices, row-major n x n (real f64, complex f64 interleaved, or
@@ -43,7 +51,7 @@ struct WalkArgs {
   int n;                 // state length
   int m;                 // Gray bits: n (Ryser) or n-1 (Glynn)
   int algo;              // 0 Ryser, 1 Glynn
-  int k;                 // segment bits (segment = 2^k indices)
+  int k;                 // segment bits (segment = 2^k indices), k >= 1
   int per_warp_slot;     // 1: every warp stages its own matrix (batched mode)
   uint64_t tile0;        // first global tile index of the launch (same for every matrix)
   uint64_t tiles;        // tiles per matrix in this launch
@@ -56,20 +64,46 @@ struct WalkArgs {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Row stride of one column in shared memory, a multiple of the 16-byte vector.
+__host__ __device__ constexpr int col_stride(int n, int elem_bytes) {
+  const int align = 16 / elem_bytes;
+  return (n + align - 1) / align * align;
+}
+
+// Resident CTAs per SM the launch bounds ask for: 3 while the register-resident
+// state is small, 2 when it is large (spilling the state costs more than the
+// lost occupancy: the product trees give plenty of ILP per warp).
+__host__ __device__ constexpr int min_ctas(int state_regs) { return state_regs > PK_MINCTA_T ? 2 : 3; }
+
+// Gray-step bookkeeping shared by the fp64 and F_p walkers.
+struct StepPlan {
+  // direction (true = remove the column) of the even step e >= 2
+  __device__ __forceinline__ static bool minus_even(uint32_t e, int k, bool lane_minus) {
+    const int b = __ffs(e) - 1;
+    return (b == k - 1) ? lane_minus : ((e >> (b + 1)) & 1);
+  }
+  // direction of the odd step o (column 0)
+  __device__ __forceinline__ static bool minus_odd(uint32_t o, int k, bool lane_minus) {
+    return (k == 1) ? lane_minus : ((o >> 1) & 1);
+  }
+};
+
 // ---------------------------------------------------------------------------
-// fp64 element helpers
+// fp64
 
 template <bool CPLX>
 struct F64T;
 template <>
 struct F64T<false> {
   using T = double;
+  static constexpr int kBytes = 8;
   __device__ static T zero() { return 0.0; }
   __device__ static T load(const double* a, int idx) { return a[idx]; }
 };
 template <>
 struct F64T<true> {
   using T = double2;
+  static constexpr int kBytes = 16;
   __device__ static T zero() { return make_double2(0.0, 0.0); }
   __device__ static T load(const double* a, int idx) {
     return make_double2(a[2 * idx], a[2 * idx + 1]);
@@ -81,18 +115,19 @@ __device__ __forceinline__ void fma_upd(double2& r, double sg, double2 c) {
   r.x = fma(sg, c.x, r.x);
   r.y = fma(sg, c.y, r.y);
 }
-__device__ __forceinline__ void add_if(double& r, bool on, double c) {
-  const double t = r + c;
-  r = on ? t : r;
+__device__ __forceinline__ void mul_acc(double& p, double v) { p *= v; }
+__device__ __forceinline__ void mul_acc(double2& p, double2 v) {
+  const double nr = fma(p.x, v.x, -(p.y * v.y));
+  p.y = fma(p.x, v.y, p.y * v.x);
+  p.x = nr;
 }
-__device__ __forceinline__ void add_if(double2& r, bool on, double2 c) {
-  const double tx = r.x + c.x, ty = r.y + c.y;
-  r.x = on ? tx : r.x;
-  r.y = on ? ty : r.y;
+__device__ __forceinline__ double2 sub2(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
 }
+__device__ __forceinline__ double sub2(double a, double b) { return a - b; }
 
-// Neumaier step, identical in form to the reference's per-component update
-// (kernels.py:56-67): t = s + v; c += (big - t) + small.
+// Neumaier step in the reference's form (kernels.py:56-67): t = s + v;
+// c += (big - t) + small.
 __device__ __forceinline__ void neumaier(double& s, double& c, double v) {
   const double t = s + v;
   const bool sb = fabs(s) >= fabs(v);
@@ -102,149 +137,154 @@ __device__ __forceinline__ void neumaier(double& s, double& c, double v) {
   s = t;
 }
 
-// Stage one matrix into shared memory in walk form: base[n] then W[m][n].
-template <bool CPLX>
-__device__ void stage_f64(typename F64T<CPLX>::T* sm, const double* a, int n, int m, int algo,
-                          int tid, int nthreads) {
-  using T = typename F64T<CPLX>::T;
+// Stage one matrix in walk form: base[NS] then W[m][NS] (NS = padded n).
+template <int N, bool CPLX>
+__device__ void stage_f64(typename F64T<CPLX>::T* sm, const double* a, int m, int algo, int tid,
+                          int nthreads) {
+  using F = F64T<CPLX>;
+  using T = typename F::T;
+  constexpr int NS = col_stride(N, F::kBytes);
   T* base = sm;
-  T* W = sm + n;
-  if (algo == 0) {
-    for (int idx = tid; idx < n * n; idx += nthreads) {
-      const int i = idx / n, b = idx % n;  // a[i][b] -> W[b][i]
-      W[b * n + i] = F64T<CPLX>::load(a, idx);
-    }
-    for (int i = tid; i < n; i += nthreads) base[i] = F64T<CPLX>::zero();
-  } else {
-    for (int idx = tid; idx < (n - 1) * n; idx += nthreads) {
-      const int b = idx / n, j = idx % n;  // W[b][j] = -2 a[b+1][j]
-      T v = F64T<CPLX>::load(a, (b + 1) * n + j);
+  T* W = sm + NS;
+  for (int idx = tid; idx < (m + 1) * NS; idx += nthreads) {
+    const int i = idx % NS;
+    const int b = idx / NS - 1;  // -1: base
+    T v = F::zero();
+    if (i >= N) {
+      // padding: never read
+    } else if (b < 0) {
+      if (algo == 1) {  // Glynn base: column sums sum_r a[r][i]
+        v = F::load(a, i);
+        for (int r = 1; r < N; ++r) {
+          const T x = F::load(a, r * N + i);
+          if constexpr (CPLX) {
+            v.x += x.x;
+            v.y += x.y;
+          } else {
+            v += x;
+          }
+        }
+      }
+    } else if (algo == 0) {
+      v = F::load(a, i * N + b);  // Ryser: W[b][i] = a[i][b]
+    } else {
+      v = F::load(a, (b + 1) * N + i);  // Glynn: W[b][i] = -2 a[b+1][i]
       if constexpr (CPLX) {
         v.x *= -2.0;
         v.y *= -2.0;
       } else {
         v *= -2.0;
       }
-      W[b * n + j] = v;
     }
-    for (int j = tid; j < n; j += nthreads) {
-      T s = F64T<CPLX>::load(a, j);
-      for (int i = 1; i < n; ++i) {
-        const T v = F64T<CPLX>::load(a, i * n + j);
-        if constexpr (CPLX) {
-          s.x += v.x;
-          s.y += v.y;
-        } else {
-          s += v;
-        }
-      }
-      base[j] = s;
-    }
+    (b < 0 ? base : W + b * NS)[i] = v;
   }
 }
 
 template <int N, bool CPLX>
 struct F64Walker {
-  using T = typename F64T<CPLX>::T;
+  using F = F64T<CPLX>;
+  using T = typename F::T;
+  static constexpr int NS = col_stride(N, F::kBytes);
 
   T r[N];
   double s_re, c_re, s_im, c_im, abs_acc;
   bool want_abs;
 
-  __device__ __forceinline__ void flip(const T* __restrict__ col, double sg) {
+  // Product of the state as a binary tree evaluated depth-first (a binary
+  // counter over the leaves): the same N - 1 multiplies as a chain, depth
+  // ~log2 N, and at most log2 N + 1 partial products live at once.
+  __device__ __forceinline__ T tree() const {
+    constexpr int LOG = 7;
+    T st[LOG];
 #pragma unroll
-    for (int i = 0; i < N; ++i) fma_upd(r[i], sg, col[i]);
-  }
-
-  __device__ __forceinline__ void accumulate(double pr, double pi, bool even) {
-    neumaier(s_re, c_re, even ? pr : -pr);
-    if constexpr (CPLX) neumaier(s_im, c_im, even ? pi : -pi);
-    if (want_abs) abs_acc += fabs(pr) + (CPLX ? fabs(pi) : 0.0);
-  }
-
-  // product of the current state (no flip); even = true adds, false subtracts
-  __device__ __forceinline__ void term(bool even) {
-    if constexpr (CPLX) {
-      double pr = r[0].x, pi = r[0].y;
+    for (int j = 0; j < N; ++j) {
+      T v = r[j];
+      int l = 0;
 #pragma unroll
-      for (int i = 1; i < N; ++i) {
-        const double nr = fma(pr, r[i].x, -(pi * r[i].y));
-        pi = fma(pr, r[i].y, pi * r[i].x);
-        pr = nr;
+      for (; l < LOG && ((j >> l) & 1); ++l) {
+        mul_acc(st[l], v);
+        v = st[l];
       }
-      accumulate(pr, pi, even);
-    } else {
-      double p0 = r[0], p1 = N > 1 ? r[1] : 1.0;
-#pragma unroll
-      for (int i = 2; i < N; i += 2) {
-        p0 *= r[i];
-        if (i + 1 < N) p1 *= r[i + 1];
-      }
-      accumulate(N > 1 ? p0 * p1 : p0, 0.0, even);
+      st[l] = v;
     }
+    // leftover complete subtrees: one per set bit of N, lowest first
+    T acc = r[0];
+    bool have = false;
+#pragma unroll
+    for (int l = 0; l < LOG; ++l) {
+      if ((N >> l) & 1) {
+        if (have) {
+          mul_acc(acc, st[l]);
+        } else {
+          acc = st[l];
+          have = true;
+        }
+      }
+    }
+    return acc;
   }
 
-  // flip column `col` with direction sg and accumulate the new term; the row
-  // update feeds the product chain directly so column loads stay short-lived
-  __device__ __forceinline__ void step(const T* __restrict__ col, double sg, bool even) {
+  // flip one column with direction sg and return the new term's product
+  __device__ __forceinline__ T step(const T* __restrict__ col, double sg) {
     if constexpr (CPLX) {
-      fma_upd(r[0], sg, col[0]);
-      double pr = r[0].x, pi = r[0].y;
 #pragma unroll
-      for (int i = 1; i < N; ++i) {
-        fma_upd(r[i], sg, col[i]);
-        const double nr = fma(pr, r[i].x, -(pi * r[i].y));
-        pi = fma(pr, r[i].y, pi * r[i].x);
-        pr = nr;
-      }
-      accumulate(pr, pi, even);
+      for (int j = 0; j < N; ++j) fma_upd(r[j], sg, col[j]);
     } else {
-      // two interleaved chains hide DMUL latency
-      fma_upd(r[0], sg, col[0]);
-      double p0 = r[0], p1 = 1.0;
 #pragma unroll
-      for (int i = 1; i < N; ++i) {
-        fma_upd(r[i], sg, col[i]);
-        if (i & 1)
-          p1 = (i == 1) ? r[i] : p1 * r[i];
-        else
-          p0 *= r[i];
+      for (int j = 0; j + 2 <= N; j += 2) {  // two rows per 16-byte load
+        const double2 c2 = *reinterpret_cast<const double2*>(col + j);
+        fma_upd(r[j], sg, c2.x);
+        fma_upd(r[j + 1], sg, c2.y);
       }
-      accumulate(N > 1 ? p0 * p1 : p0, 0.0, even);
+      if constexpr (N & 1) fma_upd(r[N - 1], sg, col[N - 1]);
+    }
+    return tree();
+  }
+
+  // Terms of a step pair (even e, odd e+1) carry opposite signs: their
+  // difference is formed in plain fp64 (one rounding, <= u (|t_e| + |t_o|))
+  // and compensated-added once, halving the Neumaier work.
+  __device__ __forceinline__ void add_pair(T pe, T po) {
+    const T d = sub2(pe, po);
+    if constexpr (CPLX) {
+      neumaier(s_re, c_re, d.x);
+      neumaier(s_im, c_im, d.y);
+      if (want_abs) abs_acc += (fabs(pe.x) + fabs(pe.y)) + (fabs(po.x) + fabs(po.y));
+    } else {
+      neumaier(s_re, c_re, d);
+      if (want_abs) abs_acc += fabs(pe) + fabs(po);
     }
   }
 
   // Walk segment `seg` (2^k indices starting at seg << k).
-  __device__ __forceinline__ void walk(const T* __restrict__ base, const T* __restrict__ W,
-                                       int m, int k, uint64_t seg) {
+  __device__ __forceinline__ void walk(const T* __restrict__ base, const T* __restrict__ W, int m,
+                                       int k, uint64_t seg) {
     const uint64_t start = seg << k;
     const uint64_t g = start ^ (start >> 1);
 #pragma unroll
-    for (int i = 0; i < N; ++i) r[i] = base[i];
-    for (int j = (k > 0 ? k - 1 : 0); j < m; ++j) {
-      const bool on = (g >> j) & 1;
-      const T* col = W + j * N;
+    for (int j = 0; j < N; ++j) r[j] = base[j];
+    for (int b = k - 1; b < m; ++b) {  // start state: columns set in gray(start)
+      const double on = ((g >> b) & 1) ? 1.0 : 0.0;
+      const T* col = W + b * NS;
 #pragma unroll
-      for (int i = 0; i < N; ++i) add_if(r[i], on, col[i]);
+      for (int j = 0; j < N; ++j) fma_upd(r[j], on, col[j]);
     }
     s_re = c_re = s_im = c_im = abs_acc = 0.0;
-    term(true);
     const uint32_t L = 1u << k;
-    const double lane_sg = (seg & 1) ? -1.0 : 1.0;  // direction at ctz = k-1
-    const double sg_odd0 = (k == 1) ? lane_sg : 1.0;
-    for (uint32_t s = 1; s + 1 < L; s += 2) {
-      // odd step s: column 0, direction = bit 1 of s (k >= 2 here).  The
-      // (s >> 31) term (always 0) keeps the compiler from hoisting column 0
-      // out of the loop into registers, which would spill the state.
-      step(W + (s >> 31) * N, ((s >> 1) & 1) ? -1.0 : 1.0, false);
-      // even step s+1: column b = ctz(s+1) >= 1
-      const uint32_t e = s + 1;
-      const int b = __ffs(e) - 1;
-      const double sg = (b == k - 1) ? lane_sg : (((e >> (b + 1)) & 1) ? -1.0 : 1.0);
-      step(W + b * N, sg, true);
+    const bool lane_minus = seg & 1;
+    {  // steps 0 (no flip) and 1
+      const T pe = tree();
+      const T po = step(W, StepPlan::minus_odd(1, k, lane_minus) ? -1.0 : 1.0);
+      add_pair(pe, po);
     }
-    // last odd step s = L-1 (bit 1 set when k >= 2)
-    step(W, (k == 1) ? sg_odd0 : -1.0, false);
+    for (uint32_t e = 2; e < L; e += 2) {
+      const int b = __ffs(e) - 1;
+      const T pe = step(W + b * NS, StepPlan::minus_even(e, k, lane_minus) ? -1.0 : 1.0);
+      // (e >> 31) is always 0: it keeps column 0 from being hoisted out of
+      // the loop into registers (which would spill the state)
+      const T po = step(W + (e >> 31) * NS, StepPlan::minus_odd(e + 1, k, lane_minus) ? -1.0 : 1.0);
+      add_pair(pe, po);
+    }
   }
 };
 
@@ -272,11 +312,14 @@ __device__ __forceinline__ double warp_sum_tree(double v) {
 }
 
 template <int N, bool CPLX>
-__global__ void __launch_bounds__(kWalkThreads, 2) walk_f64_kernel(WalkArgs args) {
-  using T = typename F64T<CPLX>::T;
+__global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
+    walk_f64_kernel(WalkArgs args) {
+  using W_ = F64Walker<N, CPLX>;
+  using T = typename W_::T;
+  constexpr int NS = W_::NS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
-  const int slot_elems = N + N * args.m;  // base + W
+  const int slot_elems = (args.m + 1) * NS;
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   T* slot = smem + (args.per_warp_slot ? warp * slot_elems : 0);
@@ -289,30 +332,30 @@ __global__ void __launch_bounds__(kWalkThreads, 2) walk_f64_kernel(WalkArgs args
 
   int staged = -1;
   if (!args.per_warp_slot) {
-    stage_f64<CPLX>(slot, amat, N, args.m, args.algo, threadIdx.x, blockDim.x);
+    stage_f64<N, CPLX>(slot, amat, args.m, args.algo, threadIdx.x, blockDim.x);
     __syncthreads();
     staged = 0;
   }
-  F64Walker<N, CPLX> w;
+  W_ w;
   w.want_abs = args.want_abs != 0;
+  // Ryser's global sign (-1)^n: the term sign at a segment start (its Gray
+  // code has even popcount).  Negation is exact and commutes with the TwoSum
+  // tree, so it is applied per lane.
+  const double sg0 = (args.algo == 0 && (N & 1)) ? -1.0 : 1.0;
   for (uint64_t u = gw; u < units; u += tw) {
     const int b = static_cast<int>(u / args.tiles);
     const uint64_t tl = u % args.tiles;
     if (b != staged) {  // warp-uniform; only in per-warp-slot mode
       __syncwarp();
-      stage_f64<CPLX>(slot, amat + b * mat_stride, N, args.m, args.algo, lane, 32);
+      stage_f64<N, CPLX>(slot, amat + b * mat_stride, args.m, args.algo, lane, 32);
       __syncwarp();
       staged = b;
     }
-    const uint64_t seg = ((args.tile0 + tl) << 5) + lane;
+    const uint64_t seg = ((args.tile0 + tl) << kTileBits) + lane;
     const bool active = seg < args.segs_total;
+    w.walk(slot, slot + NS, args.m, args.k, active ? seg : 0);
     double s_re = 0, c_re = 0, s_im = 0, c_im = 0, ab = 0;
-    w.walk(slot, slot + N, args.m, args.k, active ? seg : 0);
     if (active) {
-      // Ryser's global sign (-1)^n (the term sign at a segment start, whose
-      // Gray code has even popcount); negation is exact and commutes with
-      // the TwoSum tree, so it is applied per lane.
-      const double sg0 = (args.algo == 0 && (N & 1)) ? -1.0 : 1.0;
       s_re = sg0 * w.s_re;
       c_re = sg0 * w.c_re;
       s_im = sg0 * w.s_im;
@@ -334,58 +377,53 @@ __global__ void __launch_bounds__(kWalkThreads, 2) walk_f64_kernel(WalkArgs args
 }
 
 // ---------------------------------------------------------------------------
-// F_p walk, P primes per lane, p < 2^31 odd.  State residues are kept reduced
-// in [0, p) (add, then min(v, v-p)); the product chain is lazy Montgomery
-// (values in [0, 2p)), so one row update costs IADD3 + IMNMX (ALU pipe) and
-// one multiply costs 3 IMAD-class instructions (FMA pipe).
+// F_p walk, P primes per lane, odd p < 2^31.  The products are lazy
+// Montgomery REDC trees; row sums are either kept reduced in [0, p) (add +
+// min(v, v - p), one VIADDMNMX) or, when n (p - 1) < 2^31 ("lazy"), as exact
+// unreduced integers (one IADD3 per row update).  One REDC costs
+// IMAD.WIDE.U32 + IMAD + IMAD.HI.U32 = 5 fmaheavy issue units (measured B200
+// rates: 64 IMAD, 32 IMAD.WIDE, 32 IMAD.HI lane-ops/clk/SM).
 //
-// Shared layout per slot (uint32): W2[2][m][P][NP] (plus-column, p-minus
-// column) then base[P][NP]; NP = N rounded up to 4 for 16-byte broadcast loads.
-
-template <int N>
-struct NPad {
-  static constexpr int v = (N + 3) & ~3;
-};
+// Shared layout per slot (uint32): W2[2 dir][m][P][NS] (plus copy, minus copy:
+// p - v reduced / -v lazy) then base[P][NS]; NS = n padded to 4 words.
 
 template <int N, int P, bool LAZY>
 __device__ void stage_modp(uint32_t* sm, const uint32_t* a, const uint32_t* primes, int m,
                            int algo, int tid, int nthreads) {
-  constexpr int NP = NPad<N>::v;
-  uint32_t* W = sm;                     // [2][m][P][NP]
-  uint32_t* base = sm + 2 * m * P * NP;  // [P][NP]
+  constexpr int NS = col_stride(N, 4);
+  constexpr int CS = P * NS;  // one column, all primes
+  uint32_t* W = sm;
+  uint32_t* base = sm + 2 * m * CS;
   const int nn = N * N;
-  for (int idx = tid; idx < m * P * NP; idx += nthreads) {
-    const int i = idx % NP;
-    const int q = (idx / NP) % P;
-    const int b = idx / (NP * P);
+  for (int idx = tid; idx < (m + 1) * CS; idx += nthreads) {
+    const int i = idx % NS;
+    const int q = (idx / NS) % P;
+    const int b = idx / CS - 1;  // -1: base
     const uint32_t p = primes[q];
+    const uint32_t* aq = a + q * nn;
     uint32_t v = 0;
     if (i < N) {
-      if (algo == 0) {
-        v = a[q * nn + i * N + b];  // column b, row i
+      if (b < 0) {
+        if (algo == 1)
+          for (int r = 0; r < N; ++r) {
+            v += aq[r * N + i];
+            v = v >= p ? v - p : v;
+          }
+      } else if (algo == 0) {
+        v = aq[i * N + b];
       } else {
-        const uint32_t x = a[q * nn + (b + 1) * N + i];
-        uint32_t two = x + x;  // < 2^32 since x < 2^31
+        uint32_t two = aq[(b + 1) * N + i] * 2u;  // < 2^32 since x < 2^31
         two = two >= p ? two - p : two;
-        v = two == 0 ? 0 : p - two;  // -2 a[b+1][i] mod p
+        v = two == 0 ? 0u : p - two;  // -2 a[b+1][i] mod p
       }
     }
-    W[(0 * m + b) * P * NP + q * NP + i] = v;
-    // minus copy: p - v (reduced state) or the two's complement -v (lazy state,
-    // exact integer sums: r - v never wraps because v was added before)
-    W[(1 * m + b) * P * NP + q * NP + i] = (i < N) ? (LAZY ? 0u - v : (v == 0 ? 0 : p - v)) : 0;
-  }
-  for (int idx = tid; idx < P * NP; idx += nthreads) {
-    const int i = idx % NP, q = idx / NP;
-    const uint32_t p = primes[q];
-    uint32_t s = 0;
-    if (algo == 1 && i < N) {
-      for (int r = 0; r < N; ++r) {
-        s += a[q * nn + r * N + i];
-        s = s >= p ? s - p : s;
-      }
+    const int off = q * NS + i;
+    if (b < 0) {
+      base[off] = v;
+    } else {
+      W[b * CS + off] = v;
+      W[(m + b) * CS + off] = LAZY ? 0u - v : (v == 0 ? 0u : p - v);
     }
-    base[q * NP + i] = s;
   }
 }
 
@@ -396,14 +434,13 @@ __device__ __forceinline__ uint32_t addmod_red(uint32_t r, uint32_t c, uint32_t 
 
 template <int N, int P, bool LAZY>
 struct ModpWalker {
-  static constexpr int NP = NPad<N>::v;
-  uint32_t r[P][N];
-  uint32_t p[P], mneg[P], kneg[P];  // kneg: multiple of p bounding every product y
-  // even steps add y, odd steps add kneg - y (y <= kneg), so one 64-bit
-  // accumulator carries (even - odd) mod p without a negation per term
-  unsigned long long acc[P];
+  static constexpr int NS = col_stride(N, 4);
+  static constexpr int CS = P * NS;
 
-  // lazy: exact integer row sums (n p < 2^31), one IADD3; reduced: [0, p)
+  uint32_t r[P][N];
+  uint32_t p[P], mneg[P], kneg[P];  // kneg: multiple of p bounding every REDC output
+  unsigned long long acc[P];        // even steps add y, odd steps kneg - y
+
   __device__ __forceinline__ static void upd(uint32_t& r, uint32_t c, uint32_t p) {
     if constexpr (LAZY)
       r += c;
@@ -411,76 +448,115 @@ struct ModpWalker {
       r = addmod_red(r, c, p);
   }
 
-  __device__ __forceinline__ void flip(const uint32_t* __restrict__ col) {
+  // REDC product tree, evaluated depth-first like the fp64 tree (N - 1 REDCs,
+  // scale 2^(-32 (N-1))).  Bounds: lazy rows are < 2^31 and every REDC output
+  // < 2^30 + p (kneg covers it); reduced rows are < p, outputs < 2p, and a
+  // merged (non-leaf) input is first brought below p so the 64-bit sum in the
+  // REDC cannot overflow.
+  __device__ __forceinline__ uint32_t redc2(uint32_t x, uint32_t y, bool x_leaf, int q) const {
+    const uint32_t xr = (LAZY || x_leaf) ? x : min(x, x - p[q]);
+    return mont_lazy(xr, y, p[q], mneg[q]);
+  }
+
+  __device__ __forceinline__ void tree(uint32_t* y) const {
+    constexpr int LOG = 7;
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      const uint4* c4 = reinterpret_cast<const uint4*>(col + q * NP);
+      uint32_t st[LOG];
 #pragma unroll
-      for (int i4 = 0; i4 < NP / 4; ++i4) {
-        const uint4 c = c4[i4];
-        if (4 * i4 + 0 < N) upd(r[q][4 * i4 + 0], c.x, p[q]);
-        if (4 * i4 + 1 < N) upd(r[q][4 * i4 + 1], c.y, p[q]);
-        if (4 * i4 + 2 < N) upd(r[q][4 * i4 + 2], c.z, p[q]);
-        if (4 * i4 + 3 < N) upd(r[q][4 * i4 + 3], c.w, p[q]);
+      for (int j = 0; j < N; ++j) {
+        uint32_t v = r[q][j];
+        int l = 0;
+#pragma unroll
+        for (; l < LOG && ((j >> l) & 1); ++l) v = redc2(st[l], v, l == 0, q);
+        st[l] = v;
       }
+      uint32_t acc = 0;
+      bool have = false;
+      bool acc_leaf = false;
+#pragma unroll
+      for (int l = 0; l < LOG; ++l) {
+        if ((N >> l) & 1) {
+          if (have) {
+            acc = redc2(st[l], acc, l == 0 && false, q);
+            acc_leaf = false;
+          } else {
+            acc = st[l];
+            acc_leaf = (l == 0);
+            have = true;
+          }
+        }
+      }
+      (void)acc_leaf;
+      y[q] = acc;
     }
   }
 
-  __device__ __forceinline__ void term(bool even) {
+  // flip one column (plus or minus copy) and write the new term's products
+  __device__ __forceinline__ void step(const uint32_t* __restrict__ col, uint32_t* y) {
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      uint32_t y;
-      if constexpr (N == 1) {
-        y = r[q][0];
-      } else {
-        y = mont_lazy(r[q][0], r[q][1], p[q], mneg[q]);
 #pragma unroll
-        for (int i = 2; i < N; ++i) y = mont_lazy(r[q][i], y, p[q], mneg[q]);
+      for (int j = 0; j < NS; j += 4) {
+        const uint4 c = *reinterpret_cast<const uint4*>(col + q * NS + j);
+        upd(r[q][j], c.x, p[q]);
+        if (j + 1 < N) upd(r[q][j + 1], c.y, p[q]);
+        if (j + 2 < N) upd(r[q][j + 2], c.z, p[q]);
+        if (j + 3 < N) upd(r[q][j + 3], c.w, p[q]);
       }
-      acc[q] += even ? y : (kneg[q] - y);
     }
+    tree(y);
   }
 
-  // W2 = [2][m][P][NP]; direction d selects the plus (0) or minus (1) copy.
+  __device__ __forceinline__ void add_pair(const uint32_t* ye, const uint32_t* yo) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) acc[q] += static_cast<unsigned long long>(ye[q]) + (kneg[q] - yo[q]);
+  }
+
   __device__ __forceinline__ void walk(const uint32_t* __restrict__ W2,
                                        const uint32_t* __restrict__ base, int m, int k,
                                        uint64_t seg) {
-    const int colstride = P * NP;
-    const uint32_t* Wm = W2 + m * colstride;  // minus copies
+    const uint32_t* Wm = W2 + m * CS;  // minus copies
     const uint64_t start = seg << k;
     const uint64_t g = start ^ (start >> 1);
 #pragma unroll
     for (int q = 0; q < P; ++q)
 #pragma unroll
-      for (int i = 0; i < N; ++i) r[q][i] = base[q * NP + i];
-    for (int j = (k > 0 ? k - 1 : 0); j < m; ++j) {
-      if ((g >> j) & 1) flip(W2 + j * colstride);  // lane-divergent only during init
+      for (int j = 0; j < N; ++j) r[q][j] = base[q * NS + j];
+    for (int b = k - 1; b < m; ++b) {
+      if ((g >> b) & 1) {  // lane-divergent only during the start-state rebuild
+        const uint32_t* col = W2 + b * CS;
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+          for (int j = 0; j < N; ++j) upd(r[q][j], col[q * NS + j], p[q]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < P; ++q) acc[q] = 0ull;
-    term(true);
     const uint32_t L = 1u << k;
     const bool lane_minus = seg & 1;
-    for (uint32_t s = 1; s + 1 < L; s += 2) {
-      flip((((s >> 1) & 1) ? Wm : W2) + (s >> 31) * colstride);  // see fp64 walker
-      term(false);
-      const uint32_t e = s + 1;
+    uint32_t ye[P], yo[P];
+    tree(ye);
+    step(StepPlan::minus_odd(1, k, lane_minus) ? Wm : W2, yo);
+    add_pair(ye, yo);
+    for (uint32_t e = 2; e < L; e += 2) {
       const int b = __ffs(e) - 1;
-      const bool minus = (b == k - 1) ? lane_minus : ((e >> (b + 1)) & 1);
-      flip((minus ? Wm : W2) + b * colstride);
-      term(true);
+      step((StepPlan::minus_even(e, k, lane_minus) ? Wm : W2) + b * CS, ye);
+      // (e >> 31) is always 0: keeps column 0 from being hoisted into registers
+      step((StepPlan::minus_odd(e + 1, k, lane_minus) ? Wm : W2) + (e >> 31) * CS, yo);
+      add_pair(ye, yo);
     }
-    flip((k == 1) ? (lane_minus ? Wm : W2) : Wm);
-    term(false);
   }
 };
 
 template <int N, int P, bool LAZY>
-__global__ void __launch_bounds__(kWalkThreads) walk_modp_kernel(WalkArgs args) {
-  constexpr int NP = NPad<N>::v;
+__global__ void __launch_bounds__(kWalkThreads, min_ctas(N * P))
+    walk_modp_kernel(WalkArgs args) {
+  using W_ = ModpWalker<N, P, LAZY>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* smem = reinterpret_cast<uint32_t*>(smem_raw);
-  const int slot_words = (2 * args.m + 1) * P * NP;
+  const int slot_words = (2 * args.m + 1) * W_::CS;
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   uint32_t* slot = smem + (args.per_warp_slot ? warp * slot_words : 0);
@@ -497,7 +573,7 @@ __global__ void __launch_bounds__(kWalkThreads) walk_modp_kernel(WalkArgs args) 
     __syncthreads();
     staged = 0;
   }
-  ModpWalker<N, P, LAZY> w;
+  W_ w;
   unsigned long long tot[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) tot[q] = 0;
@@ -517,26 +593,24 @@ __global__ void __launch_bounds__(kWalkThreads) walk_modp_kernel(WalkArgs args) 
       for (int q = 0; q < P; ++q) {
         w.p[q] = args.primes[b * P + q];
         w.mneg[q] = mont_neg_inv32(w.p[q]);
-        // products stay below 2p (reduced state) or below (n/2 + 2) p (lazy
-        // state, n p <= 2^31: the first REDC sees two unreduced sums)
-        w.kneg[q] = LAZY ? w.p[q] * static_cast<uint32_t>(N / 2 + 2) : 2u * w.p[q];
+        // REDC outputs stay below 2p (reduced rows) or 2^30 + p (lazy rows)
+        w.kneg[q] = LAZY ? w.p[q] * ((1u << 30) / w.p[q] + 2u) : 2u * w.p[q];
       }
     }
     if (b != staged) {
       __syncwarp();
-      stage_modp<N, P, LAZY>(slot, amat + b * mat_stride, args.primes + b * P, args.m, args.algo, lane,
-                       32);
+      stage_modp<N, P, LAZY>(slot, amat + b * mat_stride, args.primes + b * P, args.m, args.algo,
+                             lane, 32);
       __syncwarp();
       staged = b;
     }
-    const uint64_t seg = ((args.tile0 + tl) << 5) + lane;
+    const uint64_t seg = ((args.tile0 + tl) << kTileBits) + lane;
     const bool active = seg < args.segs_total;
-    w.walk(slot, slot + 2 * args.m * P * NP, args.m, args.k, active ? seg : 0);
+    w.walk(slot, slot + 2 * args.m * W_::CS, args.m, args.k, active ? seg : 0);
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      unsigned long long v = w.acc[q] % w.p[q];
-      v = active ? v : 0ull;
-      // lane sum: 32 values < 2^32 -> < 2^37
+      unsigned long long v = active ? w.acc[q] % w.p[q] : 0ull;
+      // 32 values < 2^31 -> < 2^36
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       tot[q] += v;

@@ -3,10 +3,12 @@
 Gates (DESIGN.md "Parity"):
   * F_p residues and CRT integers: bit-exact.
   * fp64, parity kernel (exact=True): bit-identical (sum, comp) per block.
-  * fp64, production kernel: |gpu - ref| <= 2 n u S + 4 u |ref|, where
-    u = 2^-53 and S = sum over terms of |re t| + |im t| (emitted by the
-    kernel).  A flat relative tolerance is not achievable for Haar inputs
-    (SURVEY 8(c)); the reference differs from itself by more across plans.
+  * fp64, production kernel: |gpu - exact| <= 2 n u S + 4 u |exact|, where
+    u = 2^-53, S = sum over terms of |re t| + |im t| (emitted by the kernel)
+    and `exact` is the big-integer block sum (tests/exact_walk.py).  Against
+    the reference (which drifts along its sequential walk) the gate is
+    8 n u S.  A flat relative tolerance is not achievable for Haar inputs
+    (SURVEY 8(c)).
 Reference values are the committed goldens (tests/golden/) or the oracle
 (oracle/, itself pinned bit-exact to those goldens in test_oracle.py).
 """
@@ -16,6 +18,7 @@ import numpy as np
 import pytest
 
 from conftest import bits_equal, dec_c, dec_matrix, load_golden
+from exact_walk import exact_block
 from oracle import oracle
 from paper_2602_10141_b200 import engine, ensembles, geodesics, kernels, modular, perm_batch
 from paper_2602_10141_b200.domains import INTEGER, RATIONAL, REAL, PrimeField
@@ -48,20 +51,47 @@ def test_exact_kernel_bit_identical_to_reference_blocks(gpu):
     assert checked >= 80
 
 
-def test_production_kernel_blocks_within_tolerance(gpu):
+def test_production_kernel_blocks_vs_exact(gpu):
+    """Production path on every golden block, gated against the EXACT block sum.
+
+    (The reference itself drifts: e.g. haar-o n=20 [0, 5000) is off by ~2.9 n u S;
+    the GPU must stay inside 2 n u S of the exact value.)"""
     g = load_golden("f64_blocks.json")
     for case in g["cases"]:
         a = dec_matrix(case["matrix"])
         n = a.shape[0]
         for b in case["blocks"]:
-            ref = dec_c(b["sum"]) + dec_c(b["comp"])
+            if b["len"] == 0:
+                continue
+            ex = exact_block(a, b["start"], b["len"], case["algorithm"])
             s, c, ab = gpu.ryser_f64(a, case["algorithm"], b["start"], b["len"], want_abs=True)
-            got = complex(s + c)
-            assert abs(got - ref) <= tol(n, ab, ref), (case["kind"], case["algorithm"], b)
-            es, ec = kernels.ryser_partial(a, b["start"], b["len"], exact=True) \
-                if case["algorithm"] == "ryser" else \
-                kernels.glynn_partial(a, b["start"], b["len"], exact=True)
-            assert bits_equal(es, dec_c(b["sum"]))
+            assert abs(complex(s + c) - ex) <= tol(n, ab, ex), (case["kind"], case["algorithm"], b)
+            part = kernels.ryser_partial if case["algorithm"] == "ryser" else kernels.glynn_partial
+            es, ec = part(a, b["start"], b["len"], exact=True)
+            assert bits_equal(es, dec_c(b["sum"])) and bits_equal(ec, dec_c(b["comp"]))
+
+
+@pytest.mark.parametrize("kind,n,algo", [("ginibre-c", 14, "ryser"), ("haar-u", 16, "glynn"),
+                                         ("haar-o", 16, "ryser"), ("goe", 15, "glynn"),
+                                         ("haar-u", 20, "ryser")])
+def test_tile_kernel_aligned_ranges_vs_exact(gpu, kind, n, algo):
+    """Ranges made of whole tiles run in the register-resident walk kernel."""
+    a = ensembles.sample_matrix(kind, n, 77, 0)
+    span = 1 << 12  # tile span 2^(k+4) with k = 8 for these n (m >= 12)
+    for st, ln in ((0, 2 * span), (span, span), (2 * span, span + 1000)):
+        ex = exact_block(a, st, ln, algo)
+        s, c, ab = gpu.ryser_f64(a, algo, st, ln, want_abs=True)
+        assert abs(complex(s + c) - ex) <= tol(n, ab, ex), (st, ln)
+
+
+def test_small_full_permanents_vs_exact(gpu):
+    for kind, n in (("haar-u", 12), ("ginibre-r", 11), ("gue", 10), ("haar-o", 9)):
+        a = ensembles.sample_matrix(kind, n, 3, 4)
+        for algo in ("ryser", "glynn"):
+            m = n if algo == "ryser" else n - 1
+            ex = exact_block(a, 0, 1 << m, algo)
+            s, c, ab = gpu.ryser_f64(a, algo, 0, 1 << m, want_abs=True)
+            assert abs(complex(s + c) - ex) <= tol(n, ab, ex), (kind, algo)
 
 
 @pytest.mark.parametrize("kind,n,algo", [("haar-u", 20, "ryser"), ("haar-u", 22, "glynn"),
@@ -74,9 +104,11 @@ def test_full_permanent_vs_oracle(gpu, kind, n, algo):
     s, c, ab = gpu.ryser_f64(a, algo, 0, 1 << m, want_abs=True)
     got = complex(s + c) * (2.0 ** (1 - n) if algo == "glynn" else 1.0)
     scale = 2.0 ** (1 - n) if algo == "glynn" else 1.0
-    assert abs(got - ref) <= tol(n, ab * scale, ref) + 2 * n * U * ab * scale
+    # two approximations of one value: each within a few n u S of exact
+    both = 8 * n * U * ab * scale + 4 * U * abs(ref)
+    assert abs(got - ref) <= both
     api = engine.permanent(a, method=algo)
-    assert abs(complex(api) - ref) <= tol(n, ab * scale, ref) + 2 * n * U * ab * scale
+    assert abs(complex(api) - ref) <= both
     if np.isrealobj(a):
         assert isinstance(api, float)
 
@@ -84,13 +116,12 @@ def test_full_permanent_vs_oracle(gpu, kind, n, algo):
 def test_unaligned_ranges_and_ragged_pieces(gpu):
     a = ensembles.sample_matrix("ginibre-c", 16, 3, 0)
     rng = np.random.default_rng(7)
-    for _ in range(12):
-        ln = int(rng.integers(1, 1 << 15))
+    for _ in range(8):
+        ln = int(rng.integers(1, 12000))
         st = int(rng.integers(0, (1 << 16) - ln))
-        ref = oracle.block_partial(a, st, ln)
-        refv = ref[0] + ref[1]
+        ex = exact_block(a, st, ln)
         s, c, ab = gpu.ryser_f64(a, "ryser", st, ln, want_abs=True)
-        assert abs((s + c) - refv) <= tol(16, ab, refv)
+        assert abs((s + c) - ex) <= tol(16, ab, ex), (st, ln)
     s, c, _ = gpu.ryser_f64(a, "ryser", 123, 0)
     assert s == 0 and c == 0
 
@@ -115,7 +146,7 @@ def test_batch_matches_single_calls(gpu):
     for i in (0, 7, 39):
         ref = oracle.permanent(mats[i], blocks=8)
         s, c, ab = gpu.ryser_f64(mats[i], "ryser", 0, 1 << 15, want_abs=True)
-        assert abs(got[i] - ref) <= tol(15, ab, ref)
+        assert abs(got[i] - ref) <= 8 * 15 * U * ab + 4 * U * abs(ref)
     real = perm_batch(np.stack([ensembles.sample_matrix("goe", 9, 1, i) for i in range(5)]),
                       method="glynn")
     assert real.dtype == np.float64
@@ -129,7 +160,7 @@ def test_sample_permanents_c1_vs_reference(gpu):
     _, ab = perm_batch(mats, want_abs=True)
     for z, want, s in zip(got, g["c1_perms"], ab):
         ref = dec_c(want)
-        assert abs(z - ref) <= tol(20, s, ref) + 2 * 20 * U * s
+        assert abs(z - ref) <= 8 * 20 * U * s + 4 * U * abs(ref)
     goe = ensembles.sample_permanents(ensembles.EnsembleSpec("goe", 8, 20, 1), method="glynn")
     for z, want in zip(goe, g["goe8_glynn"]):
         assert abs(z - dec_c(want)) <= 1e-12 * max(1.0, abs(dec_c(want)))
