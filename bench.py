@@ -148,7 +148,7 @@ def run_reference(args):
     n = args.n
     a = headline_matrix(n)
     cores = os.cpu_count() or 1
-    bits = 21
+    bits = 23
     for _ in range(args.warmup):
         cpu_rate(a, n, cores, 16)
     rates, secs = [], 0.0

@@ -228,7 +228,13 @@ struct F64Walker {
   __device__ __forceinline__ T step(const T* __restrict__ col, double sg) {
     if constexpr (CPLX) {
 #pragma unroll
-      for (int j = 0; j < N; ++j) fma_upd(r[j], sg, col[j]);
+      for (int j = 0; j < N; ++j) {
+#ifdef PK_EXP_NOLDS  // micro-experiments only: column from registers
+        fma_upd(r[j], sg, make_double2(1e-3 * j, 1e-3));
+#else
+        fma_upd(r[j], sg, col[j]);
+#endif
+      }
     } else {
 #pragma unroll
       for (int j = 0; j + 2 <= N; j += 2) {  // two rows per 16-byte load
@@ -246,6 +252,15 @@ struct F64Walker {
   // and compensated-added once, halving the Neumaier work.
   __device__ __forceinline__ void add_pair(T pe, T po) {
     const T d = sub2(pe, po);
+#ifdef PK_EXP_NOKAHAN  // micro-experiments only (tools/micro): plain sums
+    if constexpr (CPLX) {
+      s_re += d.x;
+      s_im += d.y;
+    } else {
+      s_re += d;
+    }
+    return;
+#endif
     if constexpr (CPLX) {
       neumaier(s_re, c_re, d.x);
       neumaier(s_im, c_im, d.y);

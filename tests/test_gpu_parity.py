@@ -341,3 +341,13 @@ def test_geodesic_sweeps_and_midpoints(gpu):
     assert abs(rr - float.fromhex(g["recovery_7"])) <= 1e-6 * rr
     oc = geodesics.onset_coefficient(geodesics.sweep(7, "cycle", 101))
     assert abs(oc - float.fromhex(g["onset_7"])) <= 1e-9 * abs(oc)
+
+
+def test_schur_resumable_checkpoint(gpu, tmp_path):
+    ck = tmp_path / "s25.jsonl"
+    v, b, w, done = modular.schur_permanent_resumable(25, str(ck), chunks=8, max_chunks_this_call=3)
+    assert v is None and done == 3
+    v, b, w, done = modular.schur_permanent_resumable(25, str(ck), chunks=8)
+    assert done == 8 and v == -5198937484375
+    with pytest.raises(ValueError, match="different run"):
+        modular.schur_permanent_resumable(25, str(ck), chunks=16)

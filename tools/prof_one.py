@@ -9,6 +9,18 @@ from paper_2602_10141_b200 import _native as nat  # noqa: E402
 from tools.gpu_probe import primes_1modn, schur_res  # noqa: E402
 
 kind, n = sys.argv[1], int(sys.argv[2])
+if kind.startswith("batch"):
+    import time
+    from paper_2602_10141_b200 import ensembles, perm_batch
+    B = int(sys.argv[3]) if len(sys.argv) > 3 else 2048
+    kk = "haar-u" if kind == "batch" else "haar-o"
+    mats = ensembles.sample_batch(ensembles.EnsembleSpec(kk, n, B, 2602), 0, B)
+    perm_batch(mats[:64])
+    t = time.perf_counter()
+    perm_batch(mats)
+    dt = time.perf_counter() - t
+    print(kind, n, B, f"{dt * 1e3:.1f} ms", f"{B * n * 2.0 ** n / dt:.3e} upd/s (incl. H2D/D2H)")
+    sys.exit(0)
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 rng = np.random.default_rng(3)
 if kind.startswith("f64"):
