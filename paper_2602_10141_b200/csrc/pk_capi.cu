@@ -25,6 +25,7 @@
 #include "pk_reduce.cuh"
 #include "pk_registry.h"
 #include "pk_walk.cuh"
+#include "pk_walk_hybrid.cuh"
 
 namespace pk {
 
@@ -48,6 +49,7 @@ const char* last_error_cstr() { return g_last_error.c_str(); }
 struct Tables {
   const void* f64[2][kMaxN + 1] = {};
   const void* modp[2][kMaxP + 1][kMaxN + 1] = {};  // [lazy][P][N]
+  const void* hybrid[3][kMaxN + 1] = {};            // [PI][N], one fp64 prime
 };
 
 static const Tables& tables() {
@@ -66,6 +68,11 @@ static const Tables& tables() {
   register_modp_l1_p4_##lo(t.modp[1][4]);
     PK_FOR_EACH_RANGE(PK_REG)
 #undef PK_REG
+#define PK_REGH(lo, hi)                    \
+  register_hybrid_pi1_##lo(t.hybrid[1]);   \
+  register_hybrid_pi2_##lo(t.hybrid[2]);
+    PK_FOR_EACH_HYBRID_RANGE(PK_REGH)
+#undef PK_REGH
     return t;
   }();
   return t;
@@ -622,12 +629,20 @@ namespace pk {
 struct ModpGroup {
   int P;                       // primes in the launch group (<= kMaxP)
   bool lazy;                   // unreduced row sums (n p < 2^31) or reduced [0, p)
+  int pf = 0;                  // trailing fp64 primes (hybrid kernel, lazy only)
   std::vector<int> idx;        // indices into the caller's prime list
+  int kind() const { return pf ? 2 : (lazy ? 1 : 0); }
 };
 
 // raw -> exact residue of the fast kernel: raw * sgn0 * 2^(32 (n-1)) mod p
 static uint64_t fix_fast(uint64_t raw, uint64_t p, int n, int algo) {
   uint64_t v = mulmod_h(raw % p, pow2mod_h(32ull * (n - 1), p), p);
+  if (algo == 0 && (n & 1)) v = v == 0 ? 0 : p - v;
+  return v;
+}
+// raw -> exact residue of an fp64 (hybrid) prime: plain sum, Ryser sign only
+static uint64_t fix_fp64(uint64_t raw, uint64_t p, int n, int algo) {
+  uint64_t v = raw % p;
   if (algo == 0 && (n & 1)) v = v == 0 ? 0 : p - v;
   return v;
 }
@@ -672,15 +687,23 @@ struct ModpLaunch {
 
 static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, int P, bool lazy, int algo, int B,
                                const uint32_t* d_a, const uint32_t* d_primes, uint64_t t0,
-                               uint64_t nt, unsigned long long* d_out) {
+                               uint64_t nt, unsigned long long* d_out, int pf = 0) {
   PK_REQUIRE(p.n >= 1 && p.n <= kMaxN, kErrLimit,
              "dimension " + std::to_string(p.n) + " exceeds the GPU kernel range n <= " +
                  std::to_string(kMaxN));
   ModpLaunch L{};
-  L.fn = tables().modp[lazy ? 1 : 0][P][p.n];
-  PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing F_p kernel instantiation");
   const int per_warp = B > 1 ? 1 : 0;
-  L.smem = (2 * p.m + 1) * P * col_stride(p.n, 4) * 4 * (per_warp ? kWalkWarps : 1);
+  if (pf) {
+    const int pi = P - pf;
+    L.fn = tables().hybrid[pi][p.n];
+    PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing hybrid F_p kernel instantiation");
+    const int int_words = ((2 * p.m + 1) * pi * col_stride(p.n, 4) + 1) & ~1;
+    L.smem = (int_words * 4 + (p.m + 1) * pf * col_stride(p.n, 8) * 8) * (per_warp ? kWalkWarps : 1);
+  } else {
+    L.fn = tables().modp[lazy ? 1 : 0][P][p.n];
+    PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing F_p kernel instantiation");
+    L.smem = (2 * p.m + 1) * P * col_stride(p.n, 4) * 4 * (per_warp ? kWalkWarps : 1);
+  }
   L.occ = occupancy(c, L.fn, kWalkThreads, L.smem);
   const uint64_t units = static_cast<uint64_t>(B) * nt;
   const uint64_t ctas = (units + kWalkWarps - 1) / kWalkWarps;
@@ -707,18 +730,38 @@ static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, int P, bool lazy, int a
 // without spilling, three for n > 36.
 static int max_primes_per_lane(int n) { return n <= 36 ? kMaxP : 3; }
 
+static bool hybrid_available(int n) { return n >= kHybridMinN && n <= kMaxN; }
+
+// Launch groups: each fp64-eligible prime is paired with one Montgomery prime
+// in a hybrid (1 + 1) group while both kinds remain; the rest go in groups of
+// up to max_primes_per_lane(n) primes of one row mode.
 static std::vector<ModpGroup> group_primes(const std::vector<int>& fast, const uint64_t* primes,
                                            int n) {
   std::vector<ModpGroup> gs;
   const int pmax = max_primes_per_lane(n);
+  std::vector<int> fp, lz, red;
+  for (int k : fast) {
+    if (!lazy_prime(primes[k], n))
+      red.push_back(k);
+    else if (fp64_prime_ok(primes[k], n))
+      fp.push_back(k);
+    else
+      lz.push_back(k);
+  }
+  if (hybrid_available(n)) {
+    while (!fp.empty() && !lz.empty()) {
+      gs.push_back(ModpGroup{2, true, 1, {lz.front(), fp.front()}});
+      lz.erase(lz.begin());
+      fp.erase(fp.begin());
+    }
+  }
+  lz.insert(lz.end(), fp.begin(), fp.end());  // leftover small primes run as Montgomery
   for (int mode = 1; mode >= 0; --mode) {
-    std::vector<int> sel;
-    for (int k : fast)
-      if (lazy_prime(primes[k], n) == (mode == 1)) sel.push_back(k);
+    const std::vector<int>& sel = mode ? lz : red;
     size_t i = 0;
     while (i < sel.size()) {
       const int P = static_cast<int>(std::min<size_t>(pmax, sel.size() - i));
-      ModpGroup g{P, mode == 1, {}};
+      ModpGroup g{P, mode == 1, 0, {}};
       for (int q = 0; q < P; ++q) g.idx.push_back(sel[i + q]);
       gs.push_back(g);
       i += P;
@@ -729,12 +772,12 @@ static std::vector<ModpGroup> group_primes(const std::vector<int>& fast, const u
 
 // Upload the launch groups that share one P as a batch of B "matrices".
 static void pack_groups(const uint64_t* a, const uint64_t* primes, int n,
-                        const std::vector<ModpGroup>& gs, int P, bool lazy,
+                        const std::vector<ModpGroup>& gs, int P, int kind,
                         std::vector<uint32_t>& ha, std::vector<uint32_t>& hp,
                         std::vector<int>& which) {
   const size_t nn = static_cast<size_t>(n) * n;
   for (size_t gi = 0; gi < gs.size(); ++gi) {
-    if (gs[gi].P != P || gs[gi].lazy != lazy) continue;
+    if (gs[gi].P != P || gs[gi].kind() != kind) continue;
     which.push_back(static_cast<int>(gi));
     for (int q = 0; q < P; ++q) {
       const int k = gs[gi].idx[q];
@@ -784,21 +827,22 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
       std::lock_guard<std::mutex> g(c.mu);
       PK_CUDA(cudaSetDevice(c.dev));
       const uint64_t t0 = cut[d], t1 = cut[d + 1];
-      // fast kernel over the aligned interior, one launch per distinct (mode, P)
-      for (int lz = 1; lz >= 0; --lz)
+      // fast kernels over the aligned interior, one launch per distinct (kind, P)
+      for (int kind = 2; kind >= 0; --kind)
       for (int PP = kMaxP; PP >= 1 && t1 > t0; --PP) {
         std::vector<uint32_t> ha, hp;
         std::vector<int> which;
-        pack_groups(a, primes, n, gs, PP, lz == 1, ha, hp, which);
+        pack_groups(a, primes, n, gs, PP, kind, ha, hp, which);
         if (which.empty()) continue;
         const int B = static_cast<int>(which.size());
+        const int pf = kind == 2 ? gs[which[0]].pf : 0;
         auto* d_a = static_cast<uint32_t*>(c.a.get(ha.size() * 4));
         auto* d_p = static_cast<uint32_t*>(c.primes.get(hp.size() * 4));
         auto* d_o = static_cast<unsigned long long*>(c.modp_out.get(hp.size() * 8));
         PK_CUDA(cudaMemcpyAsync(d_a, ha.data(), ha.size() * 4, cudaMemcpyHostToDevice, c.stream));
         PK_CUDA(cudaMemcpyAsync(d_p, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice, c.stream));
         PK_CUDA(cudaMemsetAsync(d_o, 0, hp.size() * 8, c.stream));
-        ModpLaunch L = prepare_modp(c, p, PP, lz == 1, algo, B, d_a, d_p, t0, t1 - t0, d_o);
+        ModpLaunch L = prepare_modp(c, p, PP, kind >= 1, algo, B, d_a, d_p, t0, t1 - t0, d_o, pf);
         launch_walk(c, L.fn, L.grid, L.smem, L.args);
         std::vector<unsigned long long> ho(hp.size());
         PK_CUDA(cudaMemcpyAsync(ho.data(), d_o, ho.size() * 8, cudaMemcpyDeviceToHost, c.stream));
@@ -806,7 +850,9 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
         for (int bi = 0; bi < B; ++bi)
           for (int q = 0; q < PP; ++q) {
             const int k = gs[which[bi]].idx[q];
-            dev_res[d][k] = fix_fast(ho[bi * PP + q], primes[k], n, algo);
+            const bool is_fp = q >= PP - pf;
+            dev_res[d][k] = is_fp ? fix_fp64(ho[bi * PP + q], primes[k], n, algo)
+                                  : fix_fast(ho[bi * PP + q], primes[k], n, algo);
           }
       }
       if (d == 0) {
@@ -845,7 +891,7 @@ struct pk_job {
   int kind = 0;  // 0 f64, 1 modp
   DevCtx* c = nullptr;
   Plan plan;
-  int algo = 0, n = 0, P = 0, B = 1;
+  int algo = 0, n = 0, P = 0, B = 1, pf = 0;
   bool cplx = false;
   uint64_t t0 = 0, nt = 0;
   void* d_a = nullptr;
@@ -934,9 +980,8 @@ extern "C" int pk_job_modp_create(int device, const uint64_t* a, const uint64_t*
     }
     const std::vector<ModpGroup> gs = group_primes(fast, primes, n);
     for (const auto& gg : gs)
-      PK_REQUIRE(gg.P == gs.front().P && gg.lazy == gs.front().lazy, kErrArg,
-                 "resident F_p jobs need primes of one mode and a count that is a multiple "
-                 "of 4 or at most 4");
+      PK_REQUIRE(gg.P == gs.front().P && gg.kind() == gs.front().kind(), kErrArg,
+                 "resident F_p jobs need launch groups of one kind and size");
     j->plan = make_plan(n, algo, 1);
     check_range(j->plan.m, start, length);
     const Range r = make_range(j->plan, start, length);
@@ -950,7 +995,8 @@ extern "C" int pk_job_modp_create(int device, const uint64_t* a, const uint64_t*
     j->nt = r.t1 - r.t0;
     std::vector<uint32_t> ha, hp;
     std::vector<int> which;
-    pack_groups(a, primes, n, gs, j->P, gs.front().lazy, ha, hp, which);
+    pack_groups(a, primes, n, gs, j->P, gs.front().kind(), ha, hp, which);
+    j->pf = gs.front().pf;
     for (int w : which)
       for (int k : gs[w].idx) {
         j->prime_order.push_back(k);
@@ -963,7 +1009,7 @@ extern "C" int pk_job_modp_create(int device, const uint64_t* a, const uint64_t*
     PK_CUDA(cudaMalloc(&j->d_modp, hp.size() * 8));
     ModpLaunch L = prepare_modp(c, j->plan, j->P, gs.front().lazy, algo, j->B,
                                 static_cast<uint32_t*>(j->d_a),
-                                j->d_primes, j->t0, j->nt, j->d_modp);
+                                j->d_primes, j->t0, j->nt, j->d_modp, j->pf);
     j->fn = L.fn;
     j->grid = L.grid;
     j->smem = L.smem;
@@ -1017,8 +1063,11 @@ extern "C" int pk_job_run(pk_job* j, int iters, size_t flush_bytes, double* tota
     if (j->kind == 1 && out_res) {
       std::vector<unsigned long long> ho(nres);
       PK_CUDA(cudaMemcpy(ho.data(), j->d_modp, nres * 8, cudaMemcpyDeviceToHost));
-      for (size_t s = 0; s < nres; ++s)
-        out_res[j->prime_order[s]] = fix_fast(ho[s], j->primes[s], j->n, j->algo);
+      for (size_t s = 0; s < nres; ++s) {
+        const bool is_fp = static_cast<int>(s % j->P) >= j->P - j->pf;
+        out_res[j->prime_order[s]] = is_fp ? fix_fp64(ho[s], j->primes[s], j->n, j->algo)
+                                           : fix_fast(ho[s], j->primes[s], j->n, j->algo);
+      }
     }
     return 0;
   });

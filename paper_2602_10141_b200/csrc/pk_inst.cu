@@ -4,12 +4,14 @@
 // ~200 kernels build in parallel:
 //   -DPK_INST_F64 -DPK_CPLX=0|1 -DPK_N_LO=.. -DPK_N_HI=..      fp64 real/complex
 //   -DPK_INST_MODP -DPK_LAZY=0|1 -DPK_P=1..4 -DPK_N_LO=.. -DPK_N_HI=..  F_p, P primes per lane
+//   -DPK_INST_HYBRID -DPK_PI=1..2 -DPK_N_LO=.. -DPK_N_HI=..   F_p, PI Montgomery + 1 fp64 prime
 // Each object exports one registration function that stores the kernel
 // addresses for N in [PK_N_LO, PK_N_HI] into the dispatch tables (pk_capi.cu).
 #include <utility>
 
 #include "pk_registry.h"
 #include "pk_walk.cuh"
+#include "pk_walk_hybrid.cuh"
 
 #define PK_CAT2(a, b) a##b
 #define PK_CAT(a, b) PK_CAT2(a, b)
@@ -33,8 +35,17 @@ static void fill(const void** tbl, std::integer_sequence<int, I...>) {
 void PK_CAT(PK_CAT(PK_CAT(PK_CAT(PK_CAT(register_modp_l, PK_LAZY), _p), PK_P), _), PK_N_LO)(const void** tbl) {
   fill(tbl, std::make_integer_sequence<int, PK_N_HI - PK_N_LO + 1>{});
 }
+#elif defined(PK_INST_HYBRID)
+template <int... I>
+static void fill(const void** tbl, std::integer_sequence<int, I...>) {
+  ((tbl[PK_N_LO + I] = reinterpret_cast<const void*>(&walk_hybrid_kernel<PK_N_LO + I, PK_PI, 1>)),
+   ...);
+}
+void PK_CAT(PK_CAT(PK_CAT(register_hybrid_pi, PK_PI), _), PK_N_LO)(const void** tbl) {
+  fill(tbl, std::make_integer_sequence<int, PK_N_HI - PK_N_LO + 1>{});
+}
 #else
-#error "define PK_INST_F64 or PK_INST_MODP"
+#error "define PK_INST_F64, PK_INST_MODP or PK_INST_HYBRID"
 #endif
 
 }  // namespace pk

@@ -18,6 +18,14 @@ constexpr int kMaxP = 4;   // primes per lane in the F_p kernel
   void register_modp_l##lazy##_p3_##lo(const void** tbl); \
   void register_modp_l##lazy##_p4_##lo(const void** tbl);
 #define PK_DECL_MODP(lo, hi) PK_DECL_MODP1(0, lo) PK_DECL_MODP1(1, lo)
+// hybrid (Montgomery + fp64 primes) kernels exist for N in [kHybridMinN, kMaxN]
+constexpr int kHybridMinN = 17;
+#define PK_FOR_EACH_HYBRID_RANGE(X) X(17, 28) X(29, 36) X(37, 42) X(43, 48)
+#define PK_DECL_HYBRID(lo, hi)                      \
+  void register_hybrid_pi1_##lo(const void** tbl); \
+  void register_hybrid_pi2_##lo(const void** tbl);
+PK_FOR_EACH_HYBRID_RANGE(PK_DECL_HYBRID)
+#undef PK_DECL_HYBRID
 PK_FOR_EACH_RANGE(PK_DECL_F64)
 PK_FOR_EACH_RANGE(PK_DECL_MODP)
 #undef PK_DECL_F64

@@ -1,0 +1,297 @@
+// F_p walk on BOTH integer pipes: the fmaheavy pipe (IMAD REDC, lazy
+// Montgomery, pk_walk.cuh) and the otherwise idle FP64 pipe.
+//
+// The Montgomery walk is bound by the fmaheavy pipe (a REDC is 5 issue units:
+// IMAD.WIDE 2 + IMAD 1 + IMAD.HI 2) while the FP64 pipe sits idle.  Here each
+// lane carries PI primes on the Montgomery path and PF "fp64 primes" that use
+// exact double arithmetic instead:
+//   state  x  = exact unreduced row sum, 0 <= x <= n (p - 1)      (DFMA +-1: exact)
+//   modmul(x, y) = h - p rint(h / p),  h = x y exact (|h| < 2^53)  (DMUL, DFMA, DADD, DFMA)
+//   reduce(x)    = x - p rint(x / p)                              (DFMA, DADD, DFMA)
+// with rint via the 1.5 * 2^52 shift; every product stays a signed residue with
+// |y| <= p/2 + 1, so |h| <= n (p - 1)(p/2 + 1) < 2^53 whenever
+// fp64_prime_ok(p, n) (p < ~2^27 / sqrt(n): 2^24.4 at n = 36).  Two row chains
+// per prime hide the 32-cycle modmul link.  The lane's per-segment sums are
+// exact integers in double (|acc| < 2^53).  One fp64 prime costs ~5 FP64
+// instructions per row update and no fmaheavy work, so 3 Montgomery + 1 fp64
+// primes cover the same CRT bits as 4 Montgomery primes at 3/4 of the
+// fmaheavy time (n = 36: 3 x 25.8 + 24.4 >= 95 bits).
+//
+// Residues of fp64 primes are plain (no Montgomery scale); Ryser's (-1)^n is
+// applied on the host like for the Montgomery primes.
+#pragma once
+
+#include "pk_walk.cuh"
+
+namespace pk {
+
+__host__ __device__ constexpr bool fp64_prime_ok(uint64_t p, int n) {
+  // n (p - 1) ((p - 1) / 2 + 1) < 2^52 keeps h, its rounding shift and the
+  // per-segment sums exact (conservative by a factor 2)
+  return (p & 1) && p >= 3 && p < (1ull << 26) &&
+         static_cast<double>(n) * static_cast<double>(p - 1) *
+                 (static_cast<double>((p - 1) / 2) + 1.0) < 4503599627370496.0;
+}
+
+template <int N, int PF>
+struct FpPart {
+  static constexpr int NS = col_stride(N, 8);
+  static constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
+
+  double x[PF][N];
+  double p[PF], pinv[PF];
+  double acc[PF];
+
+  __device__ __forceinline__ double reduce(double v, int q) const {
+    const double qq = fma(v, pinv[q], kShift) - kShift;  // rint(v / p)
+    return fma(-qq, p[q], v);
+  }
+  __device__ __forceinline__ double modmul(double a, double y, int q) const {
+    const double h = a * y;  // exact: |h| < 2^53
+    return reduce(h, q);
+  }
+
+  // flip one column: x += sg * col (exact integers)
+  __device__ __forceinline__ void flip(const double* __restrict__ col, double sg) {
+#pragma unroll
+    for (int q = 0; q < PF; ++q)
+#pragma unroll
+      for (int j = 0; j + 2 <= N; j += 2) {
+        const double2 c = *reinterpret_cast<const double2*>(col + q * NS + j);
+        x[q][j] = fma(sg, c.x, x[q][j]);
+        x[q][j + 1] = fma(sg, c.y, x[q][j + 1]);
+      }
+    if constexpr (N & 1) {
+#pragma unroll
+      for (int q = 0; q < PF; ++q) x[q][N - 1] = fma(sg, col[q * NS + N - 1], x[q][N - 1]);
+    }
+  }
+
+  // product of the state mod p: rows dealt round-robin to kC chains (each
+  // starts with a reduce), chains joined by a small tree.  A modmul link is
+  // 4 dependent FP64 ops (~32 cycles), so the chains keep the critical path
+  // near (N / kC + log2 kC) links.
+  static constexpr int kC = N >= 16 ? 4 : (N >= 2 ? 2 : 1);
+
+  __device__ __forceinline__ void product(double* y) const {
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      double ch[kC];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int c = i % kC;
+        ch[c] = (i < kC) ? reduce(x[q][i], q) : modmul(x[q][i], ch[c], q);
+      }
+#pragma unroll
+      for (int w = 1; w < kC; w *= 2)
+#pragma unroll
+        for (int c = 0; c + w < kC; c += 2 * w) ch[c] = modmul(ch[c], ch[c + w], q);
+      y[q] = ch[0];
+    }
+  }
+};
+
+template <int N, int PI, int PF>
+__device__ void stage_hybrid(uint32_t* sm, const uint32_t* a, const uint32_t* primes, int m,
+                             int algo, int tid, int nthreads) {
+  // Montgomery part (lazy rows) in the layout of stage_modp; primes [0, PI)
+  stage_modp<N, PI, true>(sm, a, primes, m, algo, tid, nthreads);
+  // fp64 part: Wf[m][PF][NS] then basef[PF][NS] (doubles), primes [PI, PI+PF)
+  constexpr int NS4 = col_stride(N, 4);
+  constexpr int NS8 = col_stride(N, 8);
+  const int int_words = ((2 * m + 1) * PI * NS4 + 1) & ~1;
+  double* Wf = reinterpret_cast<double*>(sm + int_words);
+  double* basef = Wf + m * PF * NS8;
+  const int nn = N * N;
+  for (int idx = tid; idx < (m + 1) * PF * NS8; idx += nthreads) {
+    const int i = idx % NS8;
+    const int q = (idx / NS8) % PF;
+    const int b = idx / (PF * NS8) - 1;  // -1: base
+    const uint32_t p = primes[PI + q];
+    const uint32_t* aq = a + (PI + q) * nn;
+    uint32_t v = 0;
+    if (i < N) {
+      if (b < 0) {
+        if (algo == 1)
+          for (int r = 0; r < N; ++r) {
+            v += aq[r * N + i];
+            v = v >= p ? v - p : v;
+          }
+      } else if (algo == 0) {
+        v = aq[i * N + b];
+      } else {
+        uint32_t two = aq[(b + 1) * N + i] * 2u;
+        two = two >= p ? two - p : two;
+        v = two == 0 ? 0u : p - two;
+      }
+    }
+    (b < 0 ? basef : Wf + b * PF * NS8)[q * NS8 + i] = static_cast<double>(v);
+  }
+}
+
+template <int N, int PI, int PF>
+struct HybridWalker {
+  ModpWalker<N, PI, true> mw;
+  FpPart<N, PF> fw;
+
+  __device__ __forceinline__ void walk(const uint32_t* __restrict__ W2, const uint32_t* __restrict__ base,
+                                       const double* __restrict__ Wf, const double* __restrict__ basef,
+                                       int m, int k, uint64_t seg) {
+    constexpr int CS = ModpWalker<N, PI, true>::CS;
+    constexpr int NS8 = FpPart<N, PF>::NS;
+    const uint32_t* Wm = W2 + m * CS;
+    const uint64_t start = seg << k;
+    const uint64_t g = start ^ (start >> 1);
+#pragma unroll
+    for (int q = 0; q < PI; ++q)
+#pragma unroll
+      for (int j = 0; j < N; ++j) mw.r[q][j] = base[q * ModpWalker<N, PI, true>::NS + j];
+#pragma unroll
+    for (int q = 0; q < PF; ++q)
+#pragma unroll
+      for (int j = 0; j < N; ++j) fw.x[q][j] = basef[q * NS8 + j];
+    for (int b = k - 1; b < m; ++b) {
+      if ((g >> b) & 1) {
+        const uint32_t* col = W2 + b * CS;
+#pragma unroll
+        for (int q = 0; q < PI; ++q)
+#pragma unroll
+          for (int j = 0; j < N; ++j) mw.r[q][j] += col[q * ModpWalker<N, PI, true>::NS + j];
+        fw.flip(Wf + b * PF * NS8, 1.0);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PI; ++q) mw.acc[q] = 0ull;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) fw.acc[q] = 0.0;
+    const uint32_t L = 1u << k;
+    const bool lane_minus = seg & 1;
+    uint32_t ye[PI], yo[PI];
+    double fe[PF], fo[PF];
+    auto pair = [&]() {
+      mw.add_pair(ye, yo);
+#pragma unroll
+      for (int q = 0; q < PF; ++q) fw.acc[q] += fe[q] - fo[q];
+    };
+    // steps 0 (no flip) and 1
+    mw.tree(ye);
+    fw.product(fe);
+    {
+      const bool mi = StepPlan::minus_odd(1, k, lane_minus);
+      mw.step(mi ? Wm : W2, yo);
+      fw.flip(Wf, mi ? -1.0 : 1.0);
+      fw.product(fo);
+      pair();
+    }
+    for (uint32_t e = 2; e < L; e += 2) {
+      const int b = __ffs(e) - 1;
+      const bool me = StepPlan::minus_even(e, k, lane_minus);
+      mw.step((me ? Wm : W2) + b * CS, ye);
+      fw.flip(Wf + b * PF * NS8, me ? -1.0 : 1.0);
+      fw.product(fe);
+      const bool mo = StepPlan::minus_odd(e + 1, k, lane_minus);
+      // (e >> 31) is always 0: keeps column 0 from being hoisted into registers
+      mw.step((mo ? Wm : W2) + (e >> 31) * CS, yo);
+      fw.flip(Wf + (e >> 31) * PF * NS8, mo ? -1.0 : 1.0);
+      fw.product(fo);
+      pair();
+    }
+  }
+};
+
+template <int N, int PI, int PF>
+__global__ void __launch_bounds__(kWalkThreads, 2) walk_hybrid_kernel(WalkArgs args) {
+  constexpr int P = PI + PF;
+  constexpr int NS4 = col_stride(N, 4);
+  constexpr int NS8 = col_stride(N, 8);
+  using HW = HybridWalker<N, PI, PF>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* smem = reinterpret_cast<uint32_t*>(smem_raw);
+  const int int_words = ((2 * args.m + 1) * PI * NS4 + 1) & ~1;
+  const int slot_words = int_words + 2 * (args.m + 1) * PF * NS8;
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  uint32_t* slot = smem + (args.per_warp_slot ? warp * slot_words : 0);
+  const uint32_t* amat = static_cast<const uint32_t*>(args.a);
+  const size_t mat_stride = static_cast<size_t>(P) * N * N;
+
+  const uint64_t units = static_cast<uint64_t>(args.B) * args.tiles;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWalkWarps + warp;
+  const uint64_t tw = static_cast<uint64_t>(gridDim.x) * kWalkWarps;
+
+  int staged = -1;
+  if (!args.per_warp_slot) {
+    stage_hybrid<N, PI, PF>(slot, amat, args.primes, args.m, args.algo, threadIdx.x, blockDim.x);
+    __syncthreads();
+    staged = 0;
+  }
+  HW w;
+  unsigned long long tot[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) tot[q] = 0;
+  int cur_b = -1;
+  for (uint64_t u = gw; u < units; u += tw) {
+    const int b = static_cast<int>(u / args.tiles);
+    const uint64_t tl = u % args.tiles;
+    if (b != cur_b) {
+      if (cur_b >= 0 && lane == 0) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) atomicAdd(args.modp_out + cur_b * P + q, tot[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < P; ++q) tot[q] = 0;
+      cur_b = b;
+#pragma unroll
+      for (int q = 0; q < PI; ++q) {
+        w.mw.p[q] = args.primes[b * P + q];
+        w.mw.mneg[q] = mont_neg_inv32(w.mw.p[q]);
+        w.mw.kneg[q] = w.mw.p[q] * ((1u << 30) / w.mw.p[q] + 2u);
+      }
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const uint32_t pq = args.primes[b * P + PI + q];
+        w.fw.p[q] = static_cast<double>(pq);
+        w.fw.pinv[q] = 1.0 / static_cast<double>(pq);
+      }
+    }
+    if (b != staged) {
+      __syncwarp();
+      stage_hybrid<N, PI, PF>(slot, amat + b * mat_stride, args.primes + b * P, args.m, args.algo,
+                              lane, 32);
+      __syncwarp();
+      staged = b;
+    }
+    const uint64_t seg = ((args.tile0 + tl) << kTileBits) + lane;
+    const bool active = seg < args.segs_total;
+    const uint32_t* W2 = slot;
+    const uint32_t* base = slot + 2 * args.m * ModpWalker<N, PI, true>::CS;
+    const double* Wf = reinterpret_cast<const double*>(slot + int_words);
+    const double* basef = Wf + args.m * PF * NS8;
+    w.walk(W2, base, Wf, basef, args.m, args.k, active ? seg : 0);
+#pragma unroll
+    for (int q = 0; q < PI; ++q) {
+      unsigned long long v = active ? w.mw.acc[q] % w.mw.p[q] : 0ull;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      tot[q] += v;
+    }
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      unsigned long long v = 0;
+      if (active) {
+        const long long pq = static_cast<long long>(w.fw.p[q]);
+        const long long s = static_cast<long long>(w.fw.acc[q]) % pq;  // exact integer sum
+        v = static_cast<unsigned long long>(s < 0 ? s + pq : s);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      tot[PI + q] += v;
+    }
+  }
+  if (cur_b >= 0 && lane == 0) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) atomicAdd(args.modp_out + cur_b * P + q, tot[q]);
+  }
+}
+
+}  // namespace pk

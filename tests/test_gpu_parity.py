@@ -351,3 +351,24 @@ def test_schur_resumable_checkpoint(gpu, tmp_path):
     assert done == 8 and v == -5198937484375
     with pytest.raises(ValueError, match="different run"):
         modular.schur_permanent_resumable(25, str(ck), chunks=16)
+
+
+def test_hybrid_fp64_primes_vs_oracle(gpu):
+    """Montgomery + fp64 primes walked together (hybrid kernel) are exact."""
+    rng = np.random.default_rng(17)
+    for n in (20, 29, 36, 43):
+        basis = modular.gpu_prime_basis(n, needed_product_bits=60)
+        primes = list(basis.primes)[:4]
+        assert any(modular.fp64_prime_ok(p, n) for p in primes)
+        mats = np.stack([modular._root_matrix_u64(n, p, modular.primitive_nth_root(p, n))
+                         for p in primes])
+        for algo in ("ryser", "glynn"):
+            m = n if algo == "ryser" else n - 1
+            ln = 1 << min(m, 22)
+            st = int(rng.integers(0, (1 << m) // ln)) * ln
+            got = gpu.ryser_modp(mats, primes, algo, st, ln)
+            for k, p in enumerate(primes):
+                want = int(sum(int(x) for x in oracle.run_blocks(
+                    mats[k], [st + i * (ln // 16) for i in range(16)], [ln // 16] * 16, algo,
+                    p=p)) % p)
+                assert got[k] == want, (n, p, algo)

@@ -185,6 +185,9 @@ def test_gpu_prime_basis_properties():
             assert (p - 1) % n == 0 and modular.is_probable_prime(p)
             assert n * (p - 1) < 2 ** 31
         assert b.product > 4 * modular._perm_bound(n) + 1
+        if n >= 17:  # alternating Montgomery / fp64 primes
+            kinds = [modular.fp64_prime_ok(p, n) for p in b.primes]
+            assert kinds[:2] == [False, True]
     assert len(modular.gpu_prime_basis(36).primes) == 4
 
 
