@@ -314,6 +314,17 @@ def secondary(args, nat, modular):
     sec["modp_n32_4primes"] = {"row_updates_per_s": 2 * 4 * n * 2.0 ** n / (walk / 1e3),
                                "walk_ms": walk / 2, **job.info()}
     job.close()
+    # C2-style batched sampler (ensembles.sample_permanents): host sampling overlapped
+    # with the batched GPU walk; a 2,000-sample slice of the 50,000-sample config
+    from paper_2602_10141_b200 import ensembles
+    spec = ensembles.EnsembleSpec("haar-u", 23, 2000, SEED)
+    ensembles.sample_permanents(ensembles.EnsembleSpec("haar-u", 23, 64, SEED))
+    t0 = time.perf_counter()
+    vals = ensembles.sample_permanents(spec)
+    dt = time.perf_counter() - t0
+    sec["c2_sample_permanents"] = {"n": 23, "count": spec.count, "wall_s": dt,
+                                   "row_updates_per_s": spec.count * 23 * 2.0 ** 23 / dt,
+                                   "mean_abs_perm": float(np.mean(np.abs(vals)))}
     t0 = time.perf_counter()
     value, b, wit = modular.schur_permanent_fast(args.schur_n)
     sec["schur_exact"] = {"n": args.schur_n, "value": str(value), "primes": list(b.primes),

@@ -372,3 +372,24 @@ def test_hybrid_fp64_primes_vs_oracle(gpu):
                     mats[k], [st + i * (ln // 16) for i in range(16)], [ln // 16] * 16, algo,
                     p=p)) % p)
                 assert got[k] == want, (n, p, algo)
+
+
+@pytest.mark.parametrize("kind,n", [("gue", 24), ("goe", 24), ("ginibre-r", 22), ("haar-o", 26)])
+def test_c5_ensembles_vs_oracle(gpu, kind, n):
+    """C5: GUE/GOE/Ginibre/Haar-O permanents through the batched sampler, n up to 26."""
+    spec = ensembles.EnsembleSpec(kind, n, 3, 2602)
+    got = ensembles.sample_permanents(spec)
+    mats = ensembles.sample_batch(spec, 0, 3)
+    _, ab = perm_batch(mats, want_abs=True)
+    for i in range(3):
+        ref = oracle.permanent(mats[i], blocks=64)
+        assert abs(got[i] - ref) <= 8 * n * U * ab[i] + 4 * U * abs(ref), (kind, i)
+
+
+def test_c5_geodesic_sweep_n20_vs_oracle(gpu):
+    tr = geodesics.sweep(20, "dft", 5)
+    for t, z in zip(tr.ts, tr.perms):
+        a = geodesics.dft_geodesic(20, float(t))
+        ref = oracle.permanent(a, blocks=64)
+        s, c, ab = gpu.ryser_f64(a, "ryser", 0, 1 << 20, want_abs=True)
+        assert abs(z - ref) <= 8 * 20 * U * ab + 4 * U * abs(ref), t
