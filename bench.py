@@ -202,11 +202,13 @@ def main():
         return float(t.item())
 
     nat.require_gpu()
+    if world > 1:
+        nat.set_device_base(local)  # this rank's GPU is logical device 0 for every call
     n = args.n
     a = headline_matrix(n)
     start, length = pkdist.shard_range(n, rank, world)
     peaks = nat.measure_peaks(local)
-    job = nat.Job.f64(a, "ryser", start, length, device=local)
+    job = nat.Job.f64(a, "ryser", start, length, device=0)
     info = job.info()
 
     # ---- warm-up, then K device-timed steps (inputs resident)

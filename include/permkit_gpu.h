@@ -44,6 +44,11 @@ const char* pk_last_error(void);
 /* Number of visible CUDA devices (>= 0), or a negative status. */
 int pk_device_count(void);
 
+/* Make logical device d of every call below physical device base + d
+ * (one process per GPU: each rank sets base = LOCAL_RANK and uses device 0).
+ * Default 0.  Returns 0 or PK_ERR_ARG. */
+int pk_set_device_base(int base);
+
 /* Library version, e.g. 100 for 0.1.0. */
 int pk_version(void);
 

@@ -54,6 +54,7 @@ def _bind(lib):
     sigs = {
         "pk_last_error": (ctypes.c_char_p, []),
         "pk_device_count": (_int, []),
+        "pk_set_device_base": (_int, [_int]),
         "pk_version": (_int, []),
         "pk_max_n": (_int, []),
         "pk_ryser_f64": (_int, [_vp, _int, _int, _int, _u64, _u64, _int, P(_dbl), P(_dbl)]),
@@ -80,7 +81,7 @@ def _bind(lib):
 def exported_symbols():
     """Names of the C-ABI entry points this binding requires."""
     return [
-        "pk_last_error", "pk_device_count", "pk_version", "pk_max_n", "pk_ryser_f64",
+        "pk_last_error", "pk_device_count", "pk_set_device_base", "pk_version", "pk_max_n", "pk_ryser_f64",
         "pk_ryser_f64_blocks", "pk_ryser_f64_batch", "pk_ryser_modp", "pk_job_f64_create",
         "pk_job_modp_create", "pk_job_run", "pk_job_info", "pk_job_destroy",
         "pk_measure_peaks", "pk_peak_names", "pk_measure_latencies", "pk_latency_names",
@@ -97,6 +98,11 @@ def load_library():
                     f"{_LIB_PATH} is not built; run __graft_entry__.build() "
                     "(make -C paper_2602_10141_b200/csrc)")
             _lib = _bind(ctypes.CDLL(str(_LIB_PATH)))
+            base = os.environ.get("PERMKIT_GPU_DEVICE_BASE", "").strip()
+            if base:
+                st = _lib.pk_set_device_base(int(base))
+                if st != 0:
+                    raise GpuError(st, _lib.pk_last_error().decode(errors="replace"))
         return _lib
 
 
@@ -115,6 +121,11 @@ def device_count() -> int:
     if n < 0:
         _check(n)
     return n
+
+
+def set_device_base(base: int):
+    """Logical device 0 of every call becomes physical device ``base`` (one process per GPU)."""
+    _check(lib().pk_set_device_base(int(base)))
 
 
 def require_gpu():

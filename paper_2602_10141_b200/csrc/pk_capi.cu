@@ -119,9 +119,14 @@ static int device_count() {
   return n;
 }
 
-static DevCtx& ctx(int dev) {
+// Logical device d of every entry point is physical device base + d, so that
+// one process per GPU (torchrun) can address "its" GPU as device 0.
+static std::atomic<int> g_device_base{0};
+
+static DevCtx& ctx(int logical) {
   std::lock_guard<std::mutex> g(g_ctx_mu);
-  PK_REQUIRE(dev >= 0 && dev < 64, kErrArg, "device index out of range");
+  const int dev = logical + g_device_base.load();
+  PK_REQUIRE(logical >= 0 && dev < 64, kErrArg, "device index out of range");
   if (!g_ctx[dev]) {
     const int nd = device_count();
     PK_REQUIRE(dev < nd, kErrArg,
@@ -377,7 +382,7 @@ static void for_devices(int ndev, F&& fn) {
 }
 
 static int clamp_ndev(int ndev) {
-  const int nd = device_count();
+  const int nd = device_count() - g_device_base.load();
   PK_REQUIRE(nd > 0, kErrCuda, "no CUDA device visible");
   return std::max(1, std::min(ndev, nd));
 }
@@ -453,6 +458,17 @@ extern "C" int pk_max_n(void) { return kMaxN; }
 
 extern "C" int pk_device_count(void) {
   return pk_guard([&]() -> int { return device_count(); });
+}
+
+extern "C" int pk_set_device_base(int base) {
+  return pk_guard([&]() -> int {
+    const int nd = device_count();
+    PK_REQUIRE(base >= 0 && (base < nd || (nd == 0 && base == 0)), kErrArg,
+               "device base " + std::to_string(base) + " outside the " + std::to_string(nd) +
+                   " visible devices");
+    g_device_base.store(base);
+    return 0;
+  });
 }
 
 namespace pk {

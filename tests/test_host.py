@@ -252,3 +252,10 @@ def test_matrix_builders():
     assert matrices.lu_log_abs_det(np.zeros((3, 3)))[0] == float("-inf")
     with pytest.raises(ValueError):
         matrices.build_schur(0)
+
+
+def test_device_base_validation():
+    _native.set_device_base(0)
+    with pytest.raises(_native.GpuError):
+        _native.set_device_base(_native.device_count() + 3)
+    _native.set_device_base(0)
