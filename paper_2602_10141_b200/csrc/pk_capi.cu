@@ -50,6 +50,7 @@ struct Tables {
   const void* f64[2][kMaxN + 1] = {};
   const void* modp[2][kMaxP + 1][kMaxN + 1] = {};  // [lazy][P][N]
   const void* hybrid[3][kMaxN + 1] = {};            // [PI][N], one fp64 prime
+  const void* wide[kMaxPWide + 1][kMaxN + 1] = {};  // [P][N], Montgomery-64
 };
 
 static const Tables& tables() {
@@ -73,6 +74,12 @@ static const Tables& tables() {
   register_hybrid_pi2_##lo(t.hybrid[2]);
     PK_FOR_EACH_HYBRID_RANGE(PK_REGH)
 #undef PK_REGH
+#define PK_REGW1(lo, hi) register_wide_p1_##lo(t.wide[1]);
+#define PK_REGW2(lo, hi) register_wide_p2_##lo(t.wide[2]);
+    PK_FOR_EACH_RANGE(PK_REGW1)
+    PK_FOR_EACH_WIDE2_RANGE(PK_REGW2)
+#undef PK_REGW1
+#undef PK_REGW2
     return t;
   }();
   return t;
@@ -438,6 +445,10 @@ static uint64_t powmod_h(uint64_t b, uint64_t e, uint64_t p) {
 static uint64_t pow2mod_h(uint64_t bits_times_reps, uint64_t p) { return powmod_h(2, bits_times_reps, p); }
 
 static bool fast_prime(uint64_t p) { return (p & 1) && p >= 3 && p < (1ull << 31); }
+// odd moduli for the Montgomery-64 walk (pk_walk64.cuh)
+static bool wide_prime(uint64_t p) { return (p & 1) && p >= (1ull << 31) && p < (1ull << 62); }
+// either register-resident F_p walk
+static bool walk_prime(uint64_t p) { return fast_prime(p) || wide_prime(p); }
 // exact integer row sums fit 31 bits: n (p - 1) < 2^31
 static bool lazy_prime(uint64_t p, int n) {
   return fast_prime(p) && static_cast<uint64_t>(n) * (p - 1) < (1ull << 31);
@@ -647,7 +658,8 @@ struct ModpGroup {
   bool lazy;                   // unreduced row sums (n p < 2^31) or reduced [0, p)
   int pf = 0;                  // trailing fp64 primes (hybrid kernel, lazy only)
   std::vector<int> idx;        // indices into the caller's prime list
-  int kind() const { return pf ? 2 : (lazy ? 1 : 0); }
+  bool wide = false;           // Montgomery-64 walk: 64-bit residues, 2 output words per prime
+  int out_words() const { return wide ? 2 * P : P; }
 };
 
 // raw -> exact residue of the fast kernel: raw * sgn0 * 2^(32 (n-1)) mod p
@@ -662,9 +674,47 @@ static uint64_t fix_fp64(uint64_t raw, uint64_t p, int n, int algo) {
   if (algo == 0 && (n & 1)) v = v == 0 ? 0 : p - v;
   return v;
 }
+// (lo, hi) 128-bit counter of the wide walk -> residue: * 2^(64 n), Ryser sign
+static uint64_t fix_wide(uint64_t lo, uint64_t hi, uint64_t p, int n, int algo) {
+  const uint64_t raw = static_cast<uint64_t>(((static_cast<u128>(hi) << 64) | lo) % p);
+  uint64_t v = mulmod_h(raw, pow2mod_h(64ull * n, p), p);
+  if (algo == 0 && (n & 1)) v = v == 0 ? 0 : p - v;
+  return v;
+}
 static uint64_t fix_block(uint64_t raw, uint64_t p, int n) {
   if (!(p & 1)) return raw % p;
   return mulmod_h(raw % p, pow2mod_h(64ull * (n - 1), p), p);
+}
+// the group's residue matrices as the kernel reads them: uint32 for the 32-bit
+// kernels, uint64 for the wide walk
+static std::vector<uint8_t> pack_residues(const ModpGroup& G, const uint64_t* a, size_t nn) {
+  const size_t wb = G.wide ? 8 : 4;
+  std::vector<uint8_t> h(G.idx.size() * nn * wb);
+  size_t o = 0;
+  for (int k : G.idx)
+    for (size_t e = 0; e < nn; ++e, o += wb) {
+      if (G.wide) {
+        const uint64_t v = a[k * nn + e];
+        std::memcpy(&h[o], &v, 8);
+      } else {
+        const uint32_t v = static_cast<uint32_t>(a[k * nn + e]);
+        std::memcpy(&h[o], &v, 4);
+      }
+    }
+  return h;
+}
+// one launch group's raw output words -> residues, stored at the caller's indices
+static void decode_group(const ModpGroup& G, const unsigned long long* ho, const uint64_t* primes,
+                         int n, int algo, uint64_t* res) {
+  for (int q = 0; q < G.P; ++q) {
+    const int k = G.idx[q];
+    if (G.wide)
+      res[k] = fix_wide(ho[2 * q], ho[2 * q + 1], primes[k], n, algo);
+    else if (q >= G.P - G.pf)
+      res[k] = fix_fp64(ho[q], primes[k], n, algo);
+    else
+      res[k] = fix_fast(ho[q], primes[k], n, algo);
+  }
 }
 
 // generic walker for one modulus over pieces; returns the residue sum
@@ -701,44 +751,68 @@ struct ModpLaunch {
   WalkArgs args;
 };
 
-static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, int P, bool lazy, int algo, int B,
-                               const uint32_t* d_a, const uint32_t* d_primes, uint64_t t0,
-                               uint64_t nt, unsigned long long* d_out, int pf = 0) {
+// One launch per prime group: constants go into the kernel's grid-constant
+// parameter (args.mc); `group_primes` lists the group's moduli (the last `pf`
+// of them are fp64 primes of the hybrid kernel).
+static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, const ModpGroup& G, int algo,
+                               const void* d_a, const std::vector<uint64_t>& group_primes,
+                               uint64_t t0, uint64_t nt, unsigned long long* d_out) {
+  const bool lazy = G.lazy;
+  const int pf = G.pf;
   PK_REQUIRE(p.n >= 1 && p.n <= kMaxN, kErrLimit,
              "dimension " + std::to_string(p.n) + " exceeds the GPU kernel range n <= " +
                  std::to_string(kMaxN));
+  const int P = static_cast<int>(group_primes.size());
+  const int pi = P - pf;
   ModpLaunch L{};
-  const int per_warp = B > 1 ? 1 : 0;
-  if (pf) {
-    const int pi = P - pf;
+  if (G.wide) {
+    PK_REQUIRE(P >= 1 && P <= kMaxPWide, kErrInternal, "bad wide prime group");
+    L.fn = tables().wide[P][p.n];
+    PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing wide F_p kernel instantiation");
+    L.smem = (2 * p.m + 1) * P * col_stride(p.n, 8) * 8;
+  } else if (pf) {
     L.fn = tables().hybrid[pi][p.n];
     PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing hybrid F_p kernel instantiation");
     const int int_words = ((2 * p.m + 1) * pi * col_stride(p.n, 4) + 1) & ~1;
-    L.smem = (int_words * 4 + (p.m + 1) * pf * col_stride(p.n, 8) * 8) * (per_warp ? kWalkWarps : 1);
+    L.smem = int_words * 4 + (p.m + 1) * pf * col_stride(p.n, 8) * 8;
   } else {
     L.fn = tables().modp[lazy ? 1 : 0][P][p.n];
     PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing F_p kernel instantiation");
-    L.smem = (2 * p.m + 1) * P * col_stride(p.n, 4) * 4 * (per_warp ? kWalkWarps : 1);
+    L.smem = (2 * p.m + 1) * P * col_stride(p.n, 4) * 4;
   }
   L.occ = occupancy(c, L.fn, kWalkThreads, L.smem);
-  const uint64_t units = static_cast<uint64_t>(B) * nt;
-  const uint64_t ctas = (units + kWalkWarps - 1) / kWalkWarps;
+  const uint64_t ctas = (nt + kWalkWarps - 1) / kWalkWarps;
   L.grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(c.sms) * L.occ));
   WalkArgs& a = L.args;
   a.a = d_a;
-  a.B = B;
+  a.B = 1;
   a.n = p.n;
   a.m = p.m;
   a.algo = algo;
   a.k = p.k;
-  a.per_warp_slot = per_warp;
+  a.per_warp_slot = 0;
   a.tile0 = t0;
   a.tiles = nt;
   a.segs_total = 1ull << (p.m - p.k);
   a.partials = nullptr;
   a.modp_out = d_out;
-  a.primes = d_primes;
+  a.primes = nullptr;
   a.want_abs = 0;
+  for (int q = 0; G.wide && q < P; ++q) {
+    a.mc.p64[q] = group_primes[q];
+    a.mc.pinv64[q] = 0ull - mont_neg_inv64(group_primes[q]);
+  }
+  for (int q = 0; !G.wide && q < pi; ++q) {
+    const uint32_t pq = static_cast<uint32_t>(group_primes[q]);
+    a.mc.p[q] = pq;
+    a.mc.mneg[q] = mont_neg_inv32(pq);
+    // REDC outputs stay below 2p (reduced rows) or 2^30 + p (lazy rows)
+    a.mc.kneg[q] = lazy ? pq * ((1u << 30) / pq + 2u) : 2u * pq;
+  }
+  for (int q = 0; q < pf; ++q) {
+    a.mc.fp[q] = static_cast<double>(group_primes[pi + q]);
+    a.mc.fpinv[q] = 1.0 / a.mc.fp[q];
+  }
   return L;
 }
 
@@ -755,9 +829,11 @@ static std::vector<ModpGroup> group_primes(const std::vector<int>& fast, const u
                                            int n) {
   std::vector<ModpGroup> gs;
   const int pmax = max_primes_per_lane(n);
-  std::vector<int> fp, lz, red;
+  std::vector<int> fp, lz, red, wd;
   for (int k : fast) {
-    if (!lazy_prime(primes[k], n))
+    if (wide_prime(primes[k]))
+      wd.push_back(k);
+    else if (!lazy_prime(primes[k], n))
       red.push_back(k);
     else if (fp64_prime_ok(primes[k], n))
       fp.push_back(k);
@@ -783,24 +859,15 @@ static std::vector<ModpGroup> group_primes(const std::vector<int>& fast, const u
       i += P;
     }
   }
-  return gs;
-}
-
-// Upload the launch groups that share one P as a batch of B "matrices".
-static void pack_groups(const uint64_t* a, const uint64_t* primes, int n,
-                        const std::vector<ModpGroup>& gs, int P, int kind,
-                        std::vector<uint32_t>& ha, std::vector<uint32_t>& hp,
-                        std::vector<int>& which) {
-  const size_t nn = static_cast<size_t>(n) * n;
-  for (size_t gi = 0; gi < gs.size(); ++gi) {
-    if (gs[gi].P != P || gs[gi].kind() != kind) continue;
-    which.push_back(static_cast<int>(gi));
-    for (int q = 0; q < P; ++q) {
-      const int k = gs[gi].idx[q];
-      hp.push_back(static_cast<uint32_t>(primes[k]));
-      for (size_t e = 0; e < nn; ++e) ha.push_back(static_cast<uint32_t>(a[k * nn + e]));
-    }
+  const int wmax = n <= kWide2MaxN ? kMaxPWide : 1;
+  for (size_t i = 0; i < wd.size();) {
+    const int P = static_cast<int>(std::min<size_t>(wmax, wd.size() - i));
+    ModpGroup g{P, false, 0, {}, true};
+    for (int q = 0; q < P; ++q) g.idx.push_back(wd[i + q]);
+    gs.push_back(g);
+    i += P;
   }
+  return gs;
 }
 
 }  // namespace pk
@@ -827,7 +894,7 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
     const uint64_t nt = r.t1 - r.t0;
     std::vector<int> fast, slow;
     for (int k = 0; k < P; ++k) {
-      if (fast_prime(primes[k]) && n <= kMaxN && nt > 0)
+      if (walk_prime(primes[k]) && n <= kMaxN && nt > 0)
         fast.push_back(k);
       else
         slow.push_back(k);
@@ -843,33 +910,22 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
       std::lock_guard<std::mutex> g(c.mu);
       PK_CUDA(cudaSetDevice(c.dev));
       const uint64_t t0 = cut[d], t1 = cut[d + 1];
-      // fast kernels over the aligned interior, one launch per distinct (kind, P)
-      for (int kind = 2; kind >= 0; --kind)
-      for (int PP = kMaxP; PP >= 1 && t1 > t0; --PP) {
-        std::vector<uint32_t> ha, hp;
-        std::vector<int> which;
-        pack_groups(a, primes, n, gs, PP, kind, ha, hp, which);
-        if (which.empty()) continue;
-        const int B = static_cast<int>(which.size());
-        const int pf = kind == 2 ? gs[which[0]].pf : 0;
-        auto* d_a = static_cast<uint32_t*>(c.a.get(ha.size() * 4));
-        auto* d_p = static_cast<uint32_t*>(c.primes.get(hp.size() * 4));
-        auto* d_o = static_cast<unsigned long long*>(c.modp_out.get(hp.size() * 8));
-        PK_CUDA(cudaMemcpyAsync(d_a, ha.data(), ha.size() * 4, cudaMemcpyHostToDevice, c.stream));
-        PK_CUDA(cudaMemcpyAsync(d_p, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice, c.stream));
-        PK_CUDA(cudaMemsetAsync(d_o, 0, hp.size() * 8, c.stream));
-        ModpLaunch L = prepare_modp(c, p, PP, kind >= 1, algo, B, d_a, d_p, t0, t1 - t0, d_o, pf);
+      // fast kernels over the aligned interior, one launch per prime group
+      for (size_t gi = 0; gi < gs.size() && t1 > t0; ++gi) {
+        const ModpGroup& G = gs[gi];
+        std::vector<uint64_t> gp;
+        for (int k : G.idx) gp.push_back(primes[k]);
+        const std::vector<uint8_t> ha = pack_residues(G, a, nn);
+        void* d_a = c.a.get(ha.size());
+        auto* d_o = static_cast<unsigned long long*>(c.modp_out.get(G.out_words() * 8));
+        PK_CUDA(cudaMemcpyAsync(d_a, ha.data(), ha.size(), cudaMemcpyHostToDevice, c.stream));
+        PK_CUDA(cudaMemsetAsync(d_o, 0, G.out_words() * 8, c.stream));
+        ModpLaunch L = prepare_modp(c, p, G, algo, d_a, gp, t0, t1 - t0, d_o);
         launch_walk(c, L.fn, L.grid, L.smem, L.args);
-        std::vector<unsigned long long> ho(hp.size());
+        std::vector<unsigned long long> ho(G.out_words());
         PK_CUDA(cudaMemcpyAsync(ho.data(), d_o, ho.size() * 8, cudaMemcpyDeviceToHost, c.stream));
         PK_CUDA(cudaStreamSynchronize(c.stream));
-        for (int bi = 0; bi < B; ++bi)
-          for (int q = 0; q < PP; ++q) {
-            const int k = gs[which[bi]].idx[q];
-            const bool is_fp = q >= PP - pf;
-            dev_res[d][k] = is_fp ? fix_fp64(ho[bi * PP + q], primes[k], n, algo)
-                                  : fix_fast(ho[bi * PP + q], primes[k], n, algo);
-          }
+        decode_group(G, ho.data(), primes, n, algo, dev_res[d].data());
       }
       if (d == 0) {
         // ragged head/tail of fast primes, and every slow modulus, on device 0
@@ -918,11 +974,13 @@ struct pk_job {
   unsigned long long* d_modp = nullptr;
   void* d_flush = nullptr;
   size_t flush_cap = 0;
-  std::vector<uint64_t> primes;
-  std::vector<int> prime_order;  // caller index for each packed slot
+  std::vector<uint64_t> prime_in;  // F_p: the caller's prime list (ModpGroup::idx refers to it)
   const void* fn = nullptr;
   int grid = 0, smem = 0, occ = 0;
   WalkArgs args{};
+  std::vector<ModpLaunch> groups;  // F_p jobs: one launch per prime group
+  std::vector<ModpGroup> gdesc;    // ... and its description (output words per group)
+  size_t out_words = 0;            // F_p: length of d_modp
 };
 
 static void job_free(pk_job* j) {
@@ -991,13 +1049,10 @@ extern "C" int pk_job_modp_create(int device, const uint64_t* a, const uint64_t*
     PK_CUDA(cudaSetDevice(c.dev));
     std::vector<int> fast;
     for (int k = 0; k < P; ++k) {
-      PK_REQUIRE(fast_prime(primes[k]), kErrArg, "resident F_p jobs need odd primes < 2^31");
+      PK_REQUIRE(walk_prime(primes[k]), kErrArg, "resident F_p jobs need odd moduli < 2^62");
       fast.push_back(k);
     }
     const std::vector<ModpGroup> gs = group_primes(fast, primes, n);
-    for (const auto& gg : gs)
-      PK_REQUIRE(gg.P == gs.front().P && gg.kind() == gs.front().kind(), kErrArg,
-                 "resident F_p jobs need launch groups of one kind and size");
     j->plan = make_plan(n, algo, 1);
     check_range(j->plan.m, start, length);
     const Range r = make_range(j->plan, start, length);
@@ -1005,32 +1060,37 @@ extern "C" int pk_job_modp_create(int device, const uint64_t* a, const uint64_t*
                "job range must be aligned to the tile span 2^(k+5)");
     j->algo = algo;
     j->n = n;
-    j->P = gs.front().P;
+    j->P = P;
     j->B = static_cast<int>(gs.size());
     j->t0 = r.t0;
     j->nt = r.t1 - r.t0;
-    std::vector<uint32_t> ha, hp;
-    std::vector<int> which;
-    pack_groups(a, primes, n, gs, j->P, gs.front().kind(), ha, hp, which);
-    j->pf = gs.front().pf;
-    for (int w : which)
-      for (int k : gs[w].idx) {
-        j->prime_order.push_back(k);
-        j->primes.push_back(primes[k]);
-      }
-    PK_CUDA(cudaMalloc(&j->d_a, ha.size() * 4));
-    PK_CUDA(cudaMemcpy(j->d_a, ha.data(), ha.size() * 4, cudaMemcpyHostToDevice));
-    PK_CUDA(cudaMalloc(&j->d_primes, hp.size() * 4));
-    PK_CUDA(cudaMemcpy(j->d_primes, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice));
-    PK_CUDA(cudaMalloc(&j->d_modp, hp.size() * 8));
-    ModpLaunch L = prepare_modp(c, j->plan, j->P, gs.front().lazy, algo, j->B,
-                                static_cast<uint32_t*>(j->d_a),
-                                j->d_primes, j->t0, j->nt, j->d_modp, j->pf);
-    j->fn = L.fn;
-    j->grid = L.grid;
-    j->smem = L.smem;
-    j->occ = L.occ;
-    j->args = L.args;
+    const size_t nn = static_cast<size_t>(n) * n;
+    std::vector<uint8_t> ha;
+    std::vector<size_t> a_off, o_off;
+    for (const auto& G : gs) {
+      a_off.push_back(ha.size());
+      o_off.push_back(j->out_words);
+      const std::vector<uint8_t> g = pack_residues(G, a, nn);
+      ha.insert(ha.end(), g.begin(), g.end());
+      j->out_words += G.out_words();
+    }
+    PK_CUDA(cudaMalloc(&j->d_a, ha.size()));
+    PK_CUDA(cudaMemcpy(j->d_a, ha.data(), ha.size(), cudaMemcpyHostToDevice));
+    PK_CUDA(cudaMalloc(&j->d_modp, j->out_words * 8));
+    for (size_t gi = 0; gi < gs.size(); ++gi) {
+      const ModpGroup& G = gs[gi];
+      std::vector<uint64_t> gp;
+      for (int k : G.idx) gp.push_back(primes[k]);
+      ModpLaunch L = prepare_modp(c, j->plan, G, algo, static_cast<uint8_t*>(j->d_a) + a_off[gi],
+                                  gp, j->t0, j->nt, j->d_modp + o_off[gi]);
+      j->groups.push_back(L);
+      j->gdesc.push_back(G);
+    }
+    j->prime_in.assign(primes, primes + P);
+    j->fn = j->groups.front().fn;
+    j->grid = j->groups.front().grid;
+    j->smem = j->groups.front().smem;
+    j->occ = j->groups.front().occ;
     *job = j.release();
     return 0;
   });
@@ -1051,13 +1111,17 @@ extern "C" int pk_job_run(pk_job* j, int iters, size_t flush_bytes, double* tota
     }
     std::vector<cudaEvent_t> ev(2 * iters + 2);
     for (auto& e : ev) PK_CUDA(cudaEventCreate(&e));
-    const size_t nres = j->kind == 1 ? j->primes.size() : 0;
+    const size_t nres = j->kind == 1 ? j->out_words : 0;
     PK_CUDA(cudaEventRecord(ev[0], c.stream));
     for (int it = 0; it < iters; ++it) {
       if (flush_bytes) PK_CUDA(cudaMemsetAsync(j->d_flush, it & 0xff, flush_bytes, c.stream));
       if (j->kind == 1) PK_CUDA(cudaMemsetAsync(j->d_modp, 0, nres * 8, c.stream));
       PK_CUDA(cudaEventRecord(ev[2 + 2 * it], c.stream));
-      launch_walk(c, j->fn, j->grid, j->smem, j->args);
+      if (j->kind == 0) {
+        launch_walk(c, j->fn, j->grid, j->smem, j->args);
+      } else {
+        for (auto& L : j->groups) launch_walk(c, L.fn, L.grid, L.smem, L.args);
+      }
       PK_CUDA(cudaEventRecord(ev[3 + 2 * it], c.stream));
       if (j->kind == 0)
         launch_reduce(c, j->d_part, 1, j->t0, j->nt, j->plan.group, j->d_groups, j->d_out);
@@ -1079,10 +1143,10 @@ extern "C" int pk_job_run(pk_job* j, int iters, size_t flush_bytes, double* tota
     if (j->kind == 1 && out_res) {
       std::vector<unsigned long long> ho(nres);
       PK_CUDA(cudaMemcpy(ho.data(), j->d_modp, nres * 8, cudaMemcpyDeviceToHost));
-      for (size_t s = 0; s < nres; ++s) {
-        const bool is_fp = static_cast<int>(s % j->P) >= j->P - j->pf;
-        out_res[j->prime_order[s]] = is_fp ? fix_fp64(ho[s], j->primes[s], j->n, j->algo)
-                                           : fix_fast(ho[s], j->primes[s], j->n, j->algo);
+      size_t s = 0;
+      for (const ModpGroup& G : j->gdesc) {
+        decode_group(G, ho.data() + s, j->prime_in.data(), j->n, j->algo, out_res);
+        s += G.out_words();
       }
     }
     return 0;
@@ -1102,7 +1166,7 @@ extern "C" int pk_job_info(pk_job* j, int64_t* info) {
     info[4] = fa.numRegs;
     info[5] = static_cast<int64_t>(fa.localSizeBytes);
     info[6] = j->smem;
-    info[7] = j->kind == 0 ? 3 : 1;
+    info[7] = j->kind == 0 ? 3 : static_cast<int64_t>(j->groups.size());
     return 0;
   });
 }

@@ -5,12 +5,14 @@
 //   -DPK_INST_F64 -DPK_CPLX=0|1 -DPK_N_LO=.. -DPK_N_HI=..      fp64 real/complex
 //   -DPK_INST_MODP -DPK_LAZY=0|1 -DPK_P=1..4 -DPK_N_LO=.. -DPK_N_HI=..  F_p, P primes per lane
 //   -DPK_INST_HYBRID -DPK_PI=1..2 -DPK_N_LO=.. -DPK_N_HI=..   F_p, PI Montgomery + 1 fp64 prime
+//   -DPK_INST_WIDE -DPK_P=1..2 -DPK_N_LO=.. -DPK_N_HI=..      F_p, wide moduli (Montgomery-64)
 // Each object exports one registration function that stores the kernel
 // addresses for N in [PK_N_LO, PK_N_HI] into the dispatch tables (pk_capi.cu).
 #include <utility>
 
 #include "pk_registry.h"
 #include "pk_walk.cuh"
+#include "pk_walk64.cuh"
 #include "pk_walk_hybrid.cuh"
 
 #define PK_CAT2(a, b) a##b
@@ -44,8 +46,16 @@ static void fill(const void** tbl, std::integer_sequence<int, I...>) {
 void PK_CAT(PK_CAT(PK_CAT(register_hybrid_pi, PK_PI), _), PK_N_LO)(const void** tbl) {
   fill(tbl, std::make_integer_sequence<int, PK_N_HI - PK_N_LO + 1>{});
 }
+#elif defined(PK_INST_WIDE)
+template <int... I>
+static void fill(const void** tbl, std::integer_sequence<int, I...>) {
+  ((tbl[PK_N_LO + I] = reinterpret_cast<const void*>(&walk_modp64_kernel<PK_N_LO + I, PK_P>)), ...);
+}
+void PK_CAT(PK_CAT(PK_CAT(register_wide_p, PK_P), _), PK_N_LO)(const void** tbl) {
+  fill(tbl, std::make_integer_sequence<int, PK_N_HI - PK_N_LO + 1>{});
+}
 #else
-#error "define PK_INST_F64, PK_INST_MODP or PK_INST_HYBRID"
+#error "define PK_INST_F64, PK_INST_MODP, PK_INST_HYBRID or PK_INST_WIDE"
 #endif
 
 }  // namespace pk

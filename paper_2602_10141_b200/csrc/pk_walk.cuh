@@ -44,6 +44,15 @@ constexpr int kWalkThreads = 128;  // 4 warps per CTA
 constexpr int kWalkWarps = kWalkThreads / 32;
 constexpr int kTileBits = 5;       // 32 segments (lanes) per warp-tile
 
+// Per-launch modulus constants (F_p kernels).  Read through a pointer into the
+// __grid_constant__ kernel parameter, they compile to uniform-register / constant
+// operands of IMAD / IMAD.HI / DFMA, costing no vector-register reads.
+struct ModConsts {
+  uint32_t p[4], mneg[4], kneg[4];  // Montgomery primes, -p^-1 mod 2^32, REDC output bound
+  double fp[2], fpinv[2];           // fp64 primes (hybrid kernel) and 1/p
+  uint64_t p64[2], pinv64[2];       // wide moduli 2^31 <= p < 2^62 and p^-1 mod 2^64
+};
+
 struct WalkArgs {
   const void* a;         // B matrices, row-major n x n (real f64, complex f64 interleaved, or
                          // P x n x n uint32 residues for F_p)
@@ -60,6 +69,13 @@ struct WalkArgs {
   unsigned long long* modp_out;  // F_p: [B][P] raw sums (< 2^64, reduced on host)
   const uint32_t* primes;        // F_p: [B][P]
   int want_abs;          // fp64: accumulate sum |term| (parity tolerance)
+  ModConsts mc;          // F_p: constants of the (single) prime group of the launch
+#ifdef PK_EXP_CCOL0
+  double col0[2 * 48];   // micro-experiment: walk column 0 in the parameter space
+#endif
+#ifdef PK_EXP_CW
+  double cw[2 * 32 * 33];  // micro-experiment: the whole walk matrix (n = 32) in the parameter space
+#endif
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -189,10 +205,17 @@ struct F64Walker {
   T r[N];
   double s_re, c_re, s_im, c_im, abs_acc;
   bool want_abs;
+#ifdef PK_EXP_CCOL0
+  const T* c0;  // column 0 in the __grid_constant__ parameter (constant-bank operands)
+#endif
+#ifdef PK_EXP_CW
+  const T* cw;  // all columns in the __grid_constant__ parameter
+#endif
 
   // Product of the state as a binary tree evaluated depth-first (a binary
   // counter over the leaves): the same N - 1 multiplies as a chain, depth
   // ~log2 N, and at most log2 N + 1 partial products live at once.
+#ifndef PK_EXP_TREE2
   __device__ __forceinline__ T tree() const {
     constexpr int LOG = 7;
     T st[LOG];
@@ -223,6 +246,44 @@ struct F64Walker {
     }
     return acc;
   }
+#endif
+
+#ifdef PK_EXP_TREE2  // micro-experiments only: two interleaved half trees
+  __device__ __forceinline__ T tree() const {
+    constexpr int H = N / 2, LOG = 7;
+    T sa[LOG], sb[LOG];
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      T va = r[j], vb = r[H + j];
+      int l = 0;
+#pragma unroll
+      for (; l < LOG && ((j >> l) & 1); ++l) {
+        mul_acc(sa[l], va);
+        mul_acc(sb[l], vb);
+        va = sa[l];
+        vb = sb[l];
+      }
+      sa[l] = va;
+      sb[l] = vb;
+    }
+    T acc = r[0];
+    bool have = false;
+#pragma unroll
+    for (int l = 0; l < LOG; ++l) {
+      if ((H >> l) & 1) {
+        mul_acc(sa[l], sb[l]);
+        if (have) {
+          mul_acc(acc, sa[l]);
+        } else {
+          acc = sa[l];
+          have = true;
+        }
+      }
+    }
+    if constexpr (N & 1) mul_acc(acc, r[N - 1]);
+    return acc;
+  }
+#endif
 
   // flip one column with direction sg and return the new term's product
   __device__ __forceinline__ T step(const T* __restrict__ col, double sg) {
@@ -292,12 +353,23 @@ struct F64Walker {
       const T po = step(W, StepPlan::minus_odd(1, k, lane_minus) ? -1.0 : 1.0);
       add_pair(pe, po);
     }
+#ifdef PK_EXP_UNROLL
+#pragma unroll 2
+#endif
     for (uint32_t e = 2; e < L; e += 2) {
       const int b = __ffs(e) - 1;
+#ifdef PK_EXP_CW
+      const T pe = step(cw + b * NS, StepPlan::minus_even(e, k, lane_minus) ? -1.0 : 1.0);
+#else
       const T pe = step(W + b * NS, StepPlan::minus_even(e, k, lane_minus) ? -1.0 : 1.0);
+#endif
       // (e >> 31) is always 0: it keeps column 0 from being hoisted out of
       // the loop into registers (which would spill the state)
+#ifdef PK_EXP_CCOL0
+      const T po = step(c0, StepPlan::minus_odd(e + 1, k, lane_minus) ? -1.0 : 1.0);
+#else
       const T po = step(W + (e >> 31) * NS, StepPlan::minus_odd(e + 1, k, lane_minus) ? -1.0 : 1.0);
+#endif
       add_pair(pe, po);
     }
   }
@@ -328,7 +400,7 @@ __device__ __forceinline__ double warp_sum_tree(double v) {
 
 template <int N, bool CPLX>
 __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
-    walk_f64_kernel(WalkArgs args) {
+    walk_f64_kernel(const __grid_constant__ WalkArgs args) {
   using W_ = F64Walker<N, CPLX>;
   using T = typename W_::T;
   constexpr int NS = W_::NS;
@@ -353,6 +425,12 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
   }
   W_ w;
   w.want_abs = args.want_abs != 0;
+#ifdef PK_EXP_CCOL0
+  w.c0 = reinterpret_cast<const T*>(args.col0);
+#endif
+#ifdef PK_EXP_CW
+  w.cw = reinterpret_cast<const T*>(args.cw);
+#endif
   // Ryser's global sign (-1)^n: the term sign at a segment start (its Gray
   // code has even popcount).  Negation is exact and commutes with the TwoSum
   // tree, so it is applied per lane.
@@ -453,8 +531,10 @@ struct ModpWalker {
   static constexpr int CS = P * NS;
 
   uint32_t r[P][N];
-  uint32_t p[P], mneg[P], kneg[P];  // kneg: multiple of p bounding every REDC output
+  const ModConsts* mc;              // p, -1/p, kneg (multiple of p bounding every REDC output)
   unsigned long long acc[P];        // even steps add y, odd steps kneg - y
+
+  __device__ __forceinline__ uint32_t p(int q) const { return mc->p[q]; }
 
   __device__ __forceinline__ static void upd(uint32_t& r, uint32_t c, uint32_t p) {
     if constexpr (LAZY)
@@ -469,8 +549,8 @@ struct ModpWalker {
   // merged (non-leaf) input is first brought below p so the 64-bit sum in the
   // REDC cannot overflow.
   __device__ __forceinline__ uint32_t redc2(uint32_t x, uint32_t y, bool x_leaf, int q) const {
-    const uint32_t xr = (LAZY || x_leaf) ? x : min(x, x - p[q]);
-    return mont_lazy(xr, y, p[q], mneg[q]);
+    const uint32_t xr = (LAZY || x_leaf) ? x : min(x, x - p(q));
+    return mont_lazy(xr, y, p(q), mc->mneg[q]);
   }
 
   __device__ __forceinline__ void tree(uint32_t* y) const {
@@ -514,10 +594,10 @@ struct ModpWalker {
 #pragma unroll
       for (int j = 0; j < NS; j += 4) {
         const uint4 c = *reinterpret_cast<const uint4*>(col + q * NS + j);
-        upd(r[q][j], c.x, p[q]);
-        if (j + 1 < N) upd(r[q][j + 1], c.y, p[q]);
-        if (j + 2 < N) upd(r[q][j + 2], c.z, p[q]);
-        if (j + 3 < N) upd(r[q][j + 3], c.w, p[q]);
+        upd(r[q][j], c.x, p(q));
+        if (j + 1 < N) upd(r[q][j + 1], c.y, p(q));
+        if (j + 2 < N) upd(r[q][j + 2], c.z, p(q));
+        if (j + 3 < N) upd(r[q][j + 3], c.w, p(q));
       }
     }
     tree(y);
@@ -525,7 +605,8 @@ struct ModpWalker {
 
   __device__ __forceinline__ void add_pair(const uint32_t* ye, const uint32_t* yo) {
 #pragma unroll
-    for (int q = 0; q < P; ++q) acc[q] += static_cast<unsigned long long>(ye[q]) + (kneg[q] - yo[q]);
+    for (int q = 0; q < P; ++q)
+      acc[q] += static_cast<unsigned long long>(ye[q]) + (mc->kneg[q] - yo[q]);
   }
 
   __device__ __forceinline__ void walk(const uint32_t* __restrict__ W2,
@@ -544,7 +625,7 @@ struct ModpWalker {
 #pragma unroll
         for (int q = 0; q < P; ++q)
 #pragma unroll
-          for (int j = 0; j < N; ++j) upd(r[q][j], col[q * NS + j], p[q]);
+          for (int j = 0; j < N; ++j) upd(r[q][j], col[q * NS + j], p(q));
       }
     }
 #pragma unroll
@@ -565,75 +646,41 @@ struct ModpWalker {
   }
 };
 
+// One prime group per launch (args.B == 1, constants in args.mc).
 template <int N, int P, bool LAZY>
 __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * P))
-    walk_modp_kernel(WalkArgs args) {
+    walk_modp_kernel(const __grid_constant__ WalkArgs args) {
   using W_ = ModpWalker<N, P, LAZY>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* smem = reinterpret_cast<uint32_t*>(smem_raw);
-  const int slot_words = (2 * args.m + 1) * W_::CS;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem_raw);
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
-  uint32_t* slot = smem + (args.per_warp_slot ? warp * slot_words : 0);
-  const uint32_t* amat = static_cast<const uint32_t*>(args.a);
-  const size_t mat_stride = static_cast<size_t>(P) * N * N;
-
-  const uint64_t units = static_cast<uint64_t>(args.B) * args.tiles;
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWalkWarps + warp;
   const uint64_t tw = static_cast<uint64_t>(gridDim.x) * kWalkWarps;
-
-  int staged = -1;
-  if (!args.per_warp_slot) {
-    stage_modp<N, P, LAZY>(slot, amat, args.primes, args.m, args.algo, threadIdx.x, blockDim.x);
-    __syncthreads();
-    staged = 0;
-  }
+  stage_modp<N, P, LAZY>(slot, static_cast<const uint32_t*>(args.a), args.mc.p, args.m, args.algo,
+                         threadIdx.x, blockDim.x);
+  __syncthreads();
   W_ w;
+  w.mc = &args.mc;
   unsigned long long tot[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) tot[q] = 0;
-  int cur_b = -1;
-  for (uint64_t u = gw; u < units; u += tw) {
-    const int b = static_cast<int>(u / args.tiles);
-    const uint64_t tl = u % args.tiles;
-    if (b != cur_b) {
-      if (cur_b >= 0 && lane == 0) {
-#pragma unroll
-        for (int q = 0; q < P; ++q) atomicAdd(args.modp_out + cur_b * P + q, tot[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < P; ++q) tot[q] = 0;
-      cur_b = b;
-#pragma unroll
-      for (int q = 0; q < P; ++q) {
-        w.p[q] = args.primes[b * P + q];
-        w.mneg[q] = mont_neg_inv32(w.p[q]);
-        // REDC outputs stay below 2p (reduced rows) or 2^30 + p (lazy rows)
-        w.kneg[q] = LAZY ? w.p[q] * ((1u << 30) / w.p[q] + 2u) : 2u * w.p[q];
-      }
-    }
-    if (b != staged) {
-      __syncwarp();
-      stage_modp<N, P, LAZY>(slot, amat + b * mat_stride, args.primes + b * P, args.m, args.algo,
-                             lane, 32);
-      __syncwarp();
-      staged = b;
-    }
+  for (uint64_t tl = gw; tl < args.tiles; tl += tw) {
     const uint64_t seg = ((args.tile0 + tl) << kTileBits) + lane;
     const bool active = seg < args.segs_total;
     w.walk(slot, slot + 2 * args.m * W_::CS, args.m, args.k, active ? seg : 0);
 #pragma unroll
     for (int q = 0; q < P; ++q) {
-      unsigned long long v = active ? w.acc[q] % w.p[q] : 0ull;
+      unsigned long long v = active ? w.acc[q] % args.mc.p[q] : 0ull;
       // 32 values < 2^31 -> < 2^36
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       tot[q] += v;
     }
   }
-  if (cur_b >= 0 && lane == 0) {
+  if (lane == 0) {
 #pragma unroll
-    for (int q = 0; q < P; ++q) atomicAdd(args.modp_out + cur_b * P + q, tot[q]);
+    for (int q = 0; q < P; ++q) atomicAdd(args.modp_out + q, tot[q]);
   }
 }
 

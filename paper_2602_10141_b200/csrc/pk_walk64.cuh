@@ -1,0 +1,277 @@
+// F_p walk for wide odd moduli 2^31 <= p < 2^62: the reference's default CRT
+// basis (59-bit primes, modular.py:25, 100-108) and any PrimeField modulus that
+// does not fit the 32-bit Montgomery kernels (domains.py:126-130).
+//
+// Same Gray skeleton as walk_modp_kernel (pk_walk.cuh): aligned 2^k-step
+// segments per lane, warp-uniform flip column from shared memory, plus / minus
+// column copies selected by the step direction, depth-first product tree.
+// Arithmetic is Montgomery with R = 2^64 and the positive inverse
+// p' = p^-1 mod 2^64:
+//     T = x y = hi 2^64 + lo,  m = lo p' mod 2^64  =>  m p = lo (mod 2^64)
+//     REDC(T) = (T - m p) / 2^64 = hi - umulhi(m, p)      in (-p, p)
+// so no low-word add or carry is needed; adding p gives (0, 2p).  Inputs below
+// 2p keep T < 4p^2 < p 2^64 (p < 2^62), so REDC outputs can feed the next
+// REDC unreduced.  One REDC = two 64-bit low products and two 64-bit high
+// products on the fmaheavy pipe (~20 issue units, against 5 for Montgomery-32).
+//
+// Row sums stay reduced in [0, p) (64-bit add + conditional subtract on the
+// ALU pipe).  Each lane accumulates its segment's signed terms exactly in 128
+// bits and folds them once per segment with one more REDC; warps combine mod p
+// and add into a 128-bit (lo, hi) counter per prime with a carry-propagating
+// atomic pair.  The host multiplies by 2^(64 n) (the tree's 2^(-64 (n-1)) and
+// the fold's 2^-64) and applies Ryser's (-1)^n.
+#pragma once
+
+#include "pk_walk.cuh"
+
+namespace pk {
+
+__device__ __forceinline__ uint64_t wmul32(uint32_t a, uint32_t b) {
+  return static_cast<uint64_t>(a) * b;  // IMAD.WIDE.U32
+}
+__device__ __forceinline__ uint32_t lo32(uint64_t v) { return static_cast<uint32_t>(v); }
+__device__ __forceinline__ uint32_t hi32(uint64_t v) { return static_cast<uint32_t>(v >> 32); }
+
+// x y = (w3 w2 w1 w0) in 32-bit words: four independent IMAD.WIDE.U32 partial
+// products (fmaheavy), the carries summed on the ALU pipe (add.cc / addc).
+// Folding carries into the 64-bit addend of the wide multiplies instead needs a
+// zero-extended register pair per addend (extra IMAD.MOV on the same pipe).
+__device__ __forceinline__ void mul128(uint64_t x, uint64_t y, uint32_t& w0, uint32_t& w1,
+                                       uint32_t& w2, uint32_t& w3) {
+  const uint64_t a = wmul32(lo32(x), lo32(y)), b = wmul32(lo32(x), hi32(y));
+  const uint64_t c = wmul32(hi32(x), lo32(y)), d = wmul32(hi32(x), hi32(y));
+  w0 = lo32(a);
+  asm("add.cc.u32 %0, %3, %4;\n\t"
+      "addc.cc.u32 %1, %5, %6;\n\t"
+      "addc.u32 %2, %7, 0;\n\t"
+      "add.cc.u32 %0, %0, %8;\n\t"
+      "addc.cc.u32 %1, %1, %9;\n\t"
+      "addc.u32 %2, %2, 0;"
+      : "=r"(w1), "=r"(w2), "=r"(w3)
+      : "r"(hi32(a)), "r"(lo32(b)), "r"(lo32(d)), "r"(hi32(b)), "r"(hi32(d)), "r"(lo32(c)),
+        "r"(hi32(c)));
+}
+
+// REDC(x y) for x, y < 2p: 9 IMAD.WIDE.U32 + 2 IMAD (~20 fmaheavy issue units)
+// and ~17 ALU carry adds (__umul64hi lowers to ~30 fmaheavy units).
+__device__ __forceinline__ uint64_t redc64_lazy(uint64_t x, uint64_t y, uint64_t p,
+                                                uint64_t pinv) {
+  uint32_t l0, l1, h0, h1;
+  mul128(x, y, l0, l1, h0, h1);
+  // m = lo p' mod 2^64
+  const uint64_t u0 = wmul32(l0, lo32(pinv));
+  const uint32_t m1 = hi32(u0) + l0 * hi32(pinv) + l1 * lo32(pinv);
+  const uint64_t m = (static_cast<uint64_t>(m1) << 32) | lo32(u0);
+  // high word of m p (its low word equals lo by construction)
+  uint32_t s0, s1, t0, t1;
+  mul128(m, p, s0, s1, t0, t1);
+  const uint64_t hi = (static_cast<uint64_t>(h1) << 32) | h0;
+  const uint64_t t = (static_cast<uint64_t>(t1) << 32) | t0;
+  return hi - t + p;  // (0, 2p)
+}
+
+__device__ __forceinline__ uint64_t min_u64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// (hi 2^64 + lo) 2^-64 mod p in [0, p), for hi < p
+__device__ __forceinline__ uint64_t fold128(uint64_t lo, uint64_t hi, uint64_t p, uint64_t pinv) {
+  const uint64_t t = __umul64hi(lo * pinv, p);
+  return hi >= t ? hi - t : hi - t + p;
+}
+
+// Shared layout per slot (uint64): W2[2 dir][m][P][NS] then base[P][NS], NS = n
+// padded to 2 words (16-byte column loads).
+template <int N, int P>
+__device__ void stage_modp64(uint64_t* sm, const uint64_t* a, const uint64_t* primes, int m,
+                             int algo, int tid, int nthreads) {
+  constexpr int NS = col_stride(N, 8);
+  constexpr int CS = P * NS;
+  uint64_t* W = sm;
+  uint64_t* base = sm + 2 * m * CS;
+  const int nn = N * N;
+  for (int idx = tid; idx < (m + 1) * CS; idx += nthreads) {
+    const int i = idx % NS;
+    const int q = (idx / NS) % P;
+    const int b = idx / CS - 1;  // -1: base
+    const uint64_t p = primes[q];
+    const uint64_t* aq = a + q * nn;
+    uint64_t v = 0;
+    if (i < N) {
+      if (b < 0) {
+        if (algo == 1)
+          for (int r = 0; r < N; ++r) {
+            v += aq[r * N + i];  // < 2p < 2^63
+            v = v >= p ? v - p : v;
+          }
+      } else if (algo == 0) {
+        v = aq[i * N + b];
+      } else {
+        uint64_t two = aq[(b + 1) * N + i] * 2ull;
+        two = two >= p ? two - p : two;
+        v = two == 0 ? 0ull : p - two;  // -2 a[b+1][i] mod p
+      }
+    }
+    const int off = q * NS + i;
+    if (b < 0) {
+      base[off] = v;
+    } else {
+      W[b * CS + off] = v;
+      W[(m + b) * CS + off] = v == 0 ? 0ull : p - v;
+    }
+  }
+}
+
+template <int N, int P>
+struct Modp64Walker {
+  static constexpr int NS = col_stride(N, 8);
+  static constexpr int CS = P * NS;
+
+  uint64_t r[P][N];
+  const ModConsts* mc;
+  uint64_t acc_lo[P], acc_hi[P];  // exact 128-bit sum of the segment's terms
+
+  __device__ __forceinline__ uint64_t p(int q) const { return mc->p64[q]; }
+
+  __device__ __forceinline__ static void upd(uint64_t& r, uint64_t c, uint64_t p) {
+    const uint64_t v = r + c;  // < 2p < 2^63
+    r = min_u64(v, v - p);
+  }
+
+  __device__ __forceinline__ void tree(uint64_t* y) const {
+    constexpr int LOG = 7;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      uint64_t st[LOG];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        uint64_t v = r[q][j];
+        int l = 0;
+#pragma unroll
+        for (; l < LOG && ((j >> l) & 1); ++l) v = redc64_lazy(st[l], v, p(q), mc->pinv64[q]);
+        st[l] = v;
+      }
+      uint64_t acc = 0;
+      bool have = false;
+#pragma unroll
+      for (int l = 0; l < LOG; ++l) {
+        if ((N >> l) & 1) {
+          if (have) {
+            acc = redc64_lazy(st[l], acc, p(q), mc->pinv64[q]);
+          } else {
+            acc = st[l];
+            have = true;
+          }
+        }
+      }
+      y[q] = acc;  // < 2p
+    }
+  }
+
+  __device__ __forceinline__ void step(const uint64_t* __restrict__ col, uint64_t* y) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+#pragma unroll
+      for (int j = 0; j < NS; j += 2) {
+        const ulonglong2 c = *reinterpret_cast<const ulonglong2*>(col + q * NS + j);
+        upd(r[q][j], c.x, p(q));
+        if (j + 1 < N) upd(r[q][j + 1], c.y, p(q));
+      }
+    }
+    tree(y);
+  }
+
+  // even steps add y, odd steps add 2p - y (both < 2p + 1 <= 2^63)
+  __device__ __forceinline__ void add_pair(const uint64_t* ye, const uint64_t* yo) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const uint64_t v = ye[q] + (2 * p(q) - yo[q]);  // < 4p < 2^64
+      const uint64_t lo = acc_lo[q] + v;
+      acc_hi[q] += lo < v ? 1ull : 0ull;
+      acc_lo[q] = lo;
+    }
+  }
+
+  __device__ __forceinline__ void walk(const uint64_t* __restrict__ W2,
+                                       const uint64_t* __restrict__ base, int m, int k,
+                                       uint64_t seg) {
+    const uint64_t* Wm = W2 + m * CS;
+    const uint64_t start = seg << k;
+    const uint64_t g = start ^ (start >> 1);
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+      for (int j = 0; j < N; ++j) r[q][j] = base[q * NS + j];
+    for (int b = k - 1; b < m; ++b) {
+      if ((g >> b) & 1) {
+        const uint64_t* col = W2 + b * CS;
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+          for (int j = 0; j < N; ++j) upd(r[q][j], col[q * NS + j], p(q));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < P; ++q) acc_lo[q] = acc_hi[q] = 0ull;
+    const uint32_t L = 1u << k;
+    const bool lane_minus = seg & 1;
+    uint64_t ye[P], yo[P];
+    tree(ye);
+    step(StepPlan::minus_odd(1, k, lane_minus) ? Wm : W2, yo);
+    add_pair(ye, yo);
+    for (uint32_t e = 2; e < L; e += 2) {
+      const int b = __ffs(e) - 1;
+      step((StepPlan::minus_even(e, k, lane_minus) ? Wm : W2) + b * CS, ye);
+      step((StepPlan::minus_odd(e + 1, k, lane_minus) ? Wm : W2) + (e >> 31) * CS, yo);
+      add_pair(ye, yo);
+    }
+  }
+};
+
+// One wide prime group per launch; modp_out holds a (lo, hi) 128-bit counter
+// per prime of the fold2^-64-scaled residues.
+template <int N, int P>
+__global__ void __launch_bounds__(kWalkThreads, min_ctas(N * P * 2))
+    walk_modp64_kernel(const __grid_constant__ WalkArgs args) {
+  using W_ = Modp64Walker<N, P>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* slot = reinterpret_cast<uint64_t*>(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWalkWarps + warp;
+  const uint64_t tw = static_cast<uint64_t>(gridDim.x) * kWalkWarps;
+  stage_modp64<N, P>(slot, static_cast<const uint64_t*>(args.a), args.mc.p64, args.m, args.algo,
+                     threadIdx.x, blockDim.x);
+  __syncthreads();
+  W_ w;
+  w.mc = &args.mc;
+  uint64_t tot[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) tot[q] = 0;
+  for (uint64_t tl = gw; tl < args.tiles; tl += tw) {
+    const uint64_t seg = ((args.tile0 + tl) << kTileBits) + lane;
+    const bool active = seg < args.segs_total;
+    w.walk(slot, slot + 2 * args.m * W_::CS, args.m, args.k, active ? seg : 0);
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const uint64_t pq = args.mc.p64[q];
+      // acc < 2^k 4p with k <= 30, so hi < p
+      uint64_t v = active ? fold128(w.acc_lo[q], w.acc_hi[q], pq, args.mc.pinv64[q]) : 0ull;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const uint64_t o = v + __shfl_xor_sync(0xffffffffu, v, off);
+        v = min_u64(o, o - pq);
+      }
+      const uint64_t t = tot[q] + v;
+      tot[q] = min_u64(t, t - pq);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      unsigned long long* o = args.modp_out + 2 * q;
+      const unsigned long long old = atomicAdd(o, static_cast<unsigned long long>(tot[q]));
+      if (old + tot[q] < old) atomicAdd(o + 1, 1ull);
+    }
+  }
+}
+
+}  // namespace pk

@@ -39,12 +39,12 @@ struct FpPart {
   static constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
 
   double x[PF][N];
-  double p[PF], pinv[PF];
+  const ModConsts* mc;  // fp[q], fpinv[q]
   double acc[PF];
 
   __device__ __forceinline__ double reduce(double v, int q) const {
-    const double qq = fma(v, pinv[q], kShift) - kShift;  // rint(v / p)
-    return fma(-qq, p[q], v);
+    const double qq = fma(v, mc->fpinv[q], kShift) - kShift;  // rint(v / p)
+    return fma(-qq, mc->fp[q], v);
   }
   __device__ __forceinline__ double modmul(double a, double y, int q) const {
     const double h = a * y;  // exact: |h| < 2^53
@@ -199,78 +199,48 @@ struct HybridWalker {
   }
 };
 
+// One (Montgomery + fp64) prime group per launch (args.B == 1, constants in args.mc;
+// the residue matrices of the PI Montgomery primes come first, then the fp64 ones).
 template <int N, int PI, int PF>
-__global__ void __launch_bounds__(kWalkThreads, 2) walk_hybrid_kernel(WalkArgs args) {
+__global__ void __launch_bounds__(kWalkThreads, 2)
+    walk_hybrid_kernel(const __grid_constant__ WalkArgs args) {
   constexpr int P = PI + PF;
   constexpr int NS4 = col_stride(N, 4);
   constexpr int NS8 = col_stride(N, 8);
   using HW = HybridWalker<N, PI, PF>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* smem = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem_raw);
   const int int_words = ((2 * args.m + 1) * PI * NS4 + 1) & ~1;
-  const int slot_words = int_words + 2 * (args.m + 1) * PF * NS8;
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
-  uint32_t* slot = smem + (args.per_warp_slot ? warp * slot_words : 0);
-  const uint32_t* amat = static_cast<const uint32_t*>(args.a);
-  const size_t mat_stride = static_cast<size_t>(P) * N * N;
-
-  const uint64_t units = static_cast<uint64_t>(args.B) * args.tiles;
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWalkWarps + warp;
   const uint64_t tw = static_cast<uint64_t>(gridDim.x) * kWalkWarps;
-
-  int staged = -1;
-  if (!args.per_warp_slot) {
-    stage_hybrid<N, PI, PF>(slot, amat, args.primes, args.m, args.algo, threadIdx.x, blockDim.x);
-    __syncthreads();
-    staged = 0;
-  }
+  // stage_hybrid reads the group's primes as uint32 [PI Montgomery..., PF fp64...]
+  uint32_t pr[P];
+#pragma unroll
+  for (int q = 0; q < PI; ++q) pr[q] = args.mc.p[q];
+#pragma unroll
+  for (int q = 0; q < PF; ++q) pr[PI + q] = static_cast<uint32_t>(args.mc.fp[q]);
+  stage_hybrid<N, PI, PF>(slot, static_cast<const uint32_t*>(args.a), pr, args.m, args.algo,
+                          threadIdx.x, blockDim.x);
+  __syncthreads();
   HW w;
+  w.mw.mc = &args.mc;
+  w.fw.mc = &args.mc;
   unsigned long long tot[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) tot[q] = 0;
-  int cur_b = -1;
-  for (uint64_t u = gw; u < units; u += tw) {
-    const int b = static_cast<int>(u / args.tiles);
-    const uint64_t tl = u % args.tiles;
-    if (b != cur_b) {
-      if (cur_b >= 0 && lane == 0) {
-#pragma unroll
-        for (int q = 0; q < P; ++q) atomicAdd(args.modp_out + cur_b * P + q, tot[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < P; ++q) tot[q] = 0;
-      cur_b = b;
-#pragma unroll
-      for (int q = 0; q < PI; ++q) {
-        w.mw.p[q] = args.primes[b * P + q];
-        w.mw.mneg[q] = mont_neg_inv32(w.mw.p[q]);
-        w.mw.kneg[q] = w.mw.p[q] * ((1u << 30) / w.mw.p[q] + 2u);
-      }
-#pragma unroll
-      for (int q = 0; q < PF; ++q) {
-        const uint32_t pq = args.primes[b * P + PI + q];
-        w.fw.p[q] = static_cast<double>(pq);
-        w.fw.pinv[q] = 1.0 / static_cast<double>(pq);
-      }
-    }
-    if (b != staged) {
-      __syncwarp();
-      stage_hybrid<N, PI, PF>(slot, amat + b * mat_stride, args.primes + b * P, args.m, args.algo,
-                              lane, 32);
-      __syncwarp();
-      staged = b;
-    }
+  const uint32_t* W2 = slot;
+  const uint32_t* base = slot + 2 * args.m * ModpWalker<N, PI, true>::CS;
+  const double* Wf = reinterpret_cast<const double*>(slot + int_words);
+  const double* basef = Wf + args.m * PF * NS8;
+  for (uint64_t tl = gw; tl < args.tiles; tl += tw) {
     const uint64_t seg = ((args.tile0 + tl) << kTileBits) + lane;
     const bool active = seg < args.segs_total;
-    const uint32_t* W2 = slot;
-    const uint32_t* base = slot + 2 * args.m * ModpWalker<N, PI, true>::CS;
-    const double* Wf = reinterpret_cast<const double*>(slot + int_words);
-    const double* basef = Wf + args.m * PF * NS8;
     w.walk(W2, base, Wf, basef, args.m, args.k, active ? seg : 0);
 #pragma unroll
     for (int q = 0; q < PI; ++q) {
-      unsigned long long v = active ? w.mw.acc[q] % w.mw.p[q] : 0ull;
+      unsigned long long v = active ? w.mw.acc[q] % args.mc.p[q] : 0ull;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       tot[q] += v;
@@ -279,18 +249,18 @@ __global__ void __launch_bounds__(kWalkThreads, 2) walk_hybrid_kernel(WalkArgs a
     for (int q = 0; q < PF; ++q) {
       unsigned long long v = 0;
       if (active) {
-        const long long pq = static_cast<long long>(w.fw.p[q]);
-        const long long s = static_cast<long long>(w.fw.acc[q]) % pq;  // exact integer sum
-        v = static_cast<unsigned long long>(s < 0 ? s + pq : s);
+        const long long pq = static_cast<long long>(args.mc.fp[q]);
+        const long long sm = static_cast<long long>(w.fw.acc[q]) % pq;  // exact integer sum
+        v = static_cast<unsigned long long>(sm < 0 ? sm + pq : sm);
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       tot[PI + q] += v;
     }
   }
-  if (cur_b >= 0 && lane == 0) {
+  if (lane == 0) {
 #pragma unroll
-    for (int q = 0; q < P; ++q) atomicAdd(args.modp_out + cur_b * P + q, tot[q]);
+    for (int q = 0; q < P; ++q) atomicAdd(args.modp_out + q, tot[q]);
   }
 }
 

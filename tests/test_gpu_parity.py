@@ -357,9 +357,7 @@ def test_hybrid_fp64_primes_vs_oracle(gpu):
     """Montgomery + fp64 primes walked together (hybrid kernel) are exact."""
     rng = np.random.default_rng(17)
     for n in (20, 29, 36, 43):
-        basis = modular.gpu_prime_basis(n, needed_product_bits=60)
-        primes = list(basis.primes)[:4]
-        assert any(modular.fp64_prime_ok(p, n) for p in primes)
+        primes = modular.prime_pool(n, "lazy", 2) + modular.prime_pool(n, "fp64", 2)
         mats = np.stack([modular._root_matrix_u64(n, p, modular.primitive_nth_root(p, n))
                          for p in primes])
         for algo in ("ryser", "glynn"):
@@ -372,6 +370,57 @@ def test_hybrid_fp64_primes_vs_oracle(gpu):
                     mats[k], [st + i * (ln // 16) for i in range(16)], [ln // 16] * 16, algo,
                     p=p)) % p)
                 assert got[k] == want, (n, p, algo)
+
+
+def _wide_moduli(n):
+    """A 59-bit prime (reference default basis), the largest prime = 1 (mod n) below
+    2^62, and an odd composite wide modulus (Montgomery only needs odd p)."""
+    p59 = modular.find_primes(n, max_bits=59).primes[0]
+    k = ((1 << 62) - 2) // n
+    while not modular.is_probable_prime(k * n + 1):
+        k -= 1
+    return [p59, k * n + 1, 2147483647 * 2147483629]
+
+
+@pytest.mark.parametrize("n", [13, 24, 30, 33, 36])
+def test_wide_moduli_vs_oracle(gpu, n):
+    """Montgomery-64 walk (2^31 <= p < 2^62, two moduli per lane when n <= 36)."""
+    rng = np.random.default_rng(100 + n)
+    mods = _wide_moduli(n)
+    mats = np.stack([rng.integers(0, p, size=(n, n), dtype=np.uint64) for p in mods])
+
+    def want(q, algo, st, ln, parts=32):
+        lens = [ln // parts] * (parts - 1) + [ln - (parts - 1) * (ln // parts)]
+        starts = [st + i * (ln // parts) for i in range(parts)]
+        return int(sum(int(x) for x in oracle.run_blocks(mats[q], starts, lens, algo,
+                                                         p=mods[q])) % mods[q])
+
+    for algo in ("ryser", "glynn"):
+        m = n if algo == "ryser" else n - 1
+        k = max(min(m - 5, 8), m - 22)
+        ln = 1 << min(m, k + 6)  # two tiles of 32 segments: through the wide kernel
+        tiles = (1 << m) // ln
+        st = int(rng.integers(0, tiles)) * ln
+        got = gpu.ryser_modp(mats, mods, algo, st, ln)
+        for q in range(len(mods)):
+            assert got[q] == want(q, algo, st, ln), (n, mods[q], algo, st, ln)
+        if tiles >= 3:  # ragged head + aligned interior + ragged tail
+            st2 = int(rng.integers(1, tiles - 1)) * ln - 333
+            ln2 = ln + 777
+            got2 = gpu.ryser_modp(mats[:1], mods[:1], algo, st2, ln2)
+            assert got2[0] == want(0, algo, st2, ln2), (n, algo, "unaligned")
+
+
+def test_schur_default_59bit_basis_through_wide_kernel(gpu):
+    """The reference's default basis (59-bit) at n = 23, 25 against SURVEY Appendix A."""
+    v23, b23, w23 = modular.schur_permanent_exact(23)
+    assert v23 == -31152650265
+    assert [w.residue for w in w23 if w.prime == 576460752303422599] == [576460721150772334]
+    v25, _, w25 = modular.schur_permanent_exact(25)
+    assert v25 == -5198937484375
+    r25 = {w.prime: w.residue for w in w25}
+    assert r25[576460752303422801] == 576455553365938426
+    assert r25[576460752303422501] == 576455553365938126
 
 
 @pytest.mark.parametrize("kind,n", [("gue", 24), ("goe", 24), ("ginibre-r", 22), ("haar-o", 26)])

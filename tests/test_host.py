@@ -179,16 +179,27 @@ def test_crt_round_trip_and_basis_checks():
 
 
 def test_gpu_prime_basis_properties():
-    for n in (2, 13, 30, 35, 36, 37, 43, 48):
+    for n in (2, 13, 17, 30, 35, 36, 37, 41, 43, 48):
         b = modular.gpu_prime_basis(n)
         for p in b.primes:
-            assert (p - 1) % n == 0 and modular.is_probable_prime(p)
-            assert n * (p - 1) < 2 ** 31
+            assert (p - 1) % n == 0 and modular.is_probable_prime(p) and p < 2 ** 31
         assert b.product > 4 * modular._perm_bound(n) + 1
-        if n >= 17:  # alternating Montgomery / fp64 primes
-            kinds = [modular.fp64_prime_ok(p, n) for p in b.primes]
-            assert kinds[:2] == [False, True]
+        kinds = [("fp64" if modular.fp64_prime_ok(p, n) else
+                  "lazy" if n * (p - 1) < 2 ** 31 else "red") for p in b.primes]
+        cost = modular.basis_walk_seconds(n, kinds.count("red"), kinds.count("lazy"),
+                                          kinds.count("fp64"))
+        # no worse than the reference-style all-31-bit basis or an all-lazy basis
+        ref31 = len(modular.find_primes(n, max_bits=31).primes)
+        assert cost <= modular.basis_walk_seconds(n, ref31, 0, 0) + 1e-12
     assert len(modular.gpu_prime_basis(36).primes) == 4
+    # n = 36: two (lazy, fp64) hybrid pairs; n = 43: four reduced primes (3 + 1)
+    assert [modular.fp64_prime_ok(p, 36) for p in modular.gpu_prime_basis(36).primes].count(True) == 2
+    assert all(43 * (p - 1) >= 2 ** 31 for p in modular.gpu_prime_basis(43).primes)
+    assert modular._launch_groups(43, 4, 0, 0) == [("red", 3), ("red", 1)]
+    assert modular._launch_groups(36, 0, 2, 2) == [("hyb", 2), ("hyb", 2)]
+    for kind in ("reduced", "lazy", "fp64"):
+        pool = modular.prime_pool(36, kind, 3)
+        assert len(pool) == 3 and pool == sorted(pool, reverse=True)
 
 
 def test_integer_crt_primes_cover_bound():

@@ -34,6 +34,18 @@ int main(int argc, char** argv) {
   WalkArgs w{};
   w.a = da; w.B = 1; w.n = n; w.m = m; w.algo = 0; w.k = k; w.per_warp_slot = 0;
   w.tile0 = 0; w.tiles = tiles; w.segs_total = 1ull << (m - k); w.partials = dp; w.want_abs = 0;
+#ifdef PK_EXP_CW
+  for (int b = 0; b < n; ++b)
+    for (int i = 0; i < n; ++i) {  // Ryser W[b][i] = a[i][b]
+      if (CPLX) { w.cw[2 * (b * 32 + i)] = a[2 * (i * n + b)]; w.cw[2 * (b * 32 + i) + 1] = a[2 * (i * n + b) + 1]; }
+    }
+#endif
+#ifdef PK_EXP_CCOL0
+  for (int i = 0; i < n; ++i) {  // Ryser column 0 = a[:, 0]
+    if (CPLX) { w.col0[2 * i] = a[2 * (i * n)]; w.col0[2 * i + 1] = a[2 * (i * n) + 1]; }
+    else w.col0[i] = a[i * n];
+  }
+#endif
   const int grid = sms * occ;
   void* args[] = {&w};
   cudaLaunchKernel(fn, grid, kWalkThreads, args, smem, 0);
