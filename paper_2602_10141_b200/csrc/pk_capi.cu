@@ -47,7 +47,7 @@ const char* last_error_cstr() { return g_last_error.c_str(); }
 // kernel tables
 
 struct Tables {
-  const void* f64[2][kMaxN + 1] = {};
+  const void* f64[2][2][kMaxN + 1] = {};          // [cplx][column 0 in param][N]
   const void* modp[2][kMaxP + 1][kMaxN + 1] = {};  // [lazy][P][N]
   const void* hybrid[3][kMaxN + 1] = {};            // [PI][N], one fp64 prime
   const void* wide[kMaxPWide + 1][kMaxN + 1] = {};  // [P][N], Montgomery-64
@@ -57,8 +57,10 @@ static const Tables& tables() {
   static const Tables t = [] {
     Tables t;
 #define PK_REG(lo, hi)                       \
-  register_f64_c0_##lo(t.f64[0]);            \
-  register_f64_c1_##lo(t.f64[1]);            \
+  register_f64_c0_p0_##lo(t.f64[0][0]);      \
+  register_f64_c1_p0_##lo(t.f64[1][0]);      \
+  register_f64_c0_p1_##lo(t.f64[0][1]);      \
+  register_f64_c1_p1_##lo(t.f64[1][1]);      \
   register_modp_l0_p1_##lo(t.modp[0][1]);   \
   register_modp_l0_p2_##lo(t.modp[0][2]);   \
   register_modp_l0_p3_##lo(t.modp[0][3]);   \
@@ -259,14 +261,18 @@ struct F64Launch {
   WalkArgs args;
 };
 
+// h_a: the host copy of a single matrix (B == 1).  When given, walk column 0
+// goes into the kernel parameter (WalkArgs::col0) and the C0P kernel runs.
 static F64Launch prepare_f64(DevCtx& c, const Plan& p, bool cplx, int algo, int B,
                              const double* d_a, uint64_t t0, uint64_t nt, bool want_abs,
-                             double* d_partials) {
+                             double* d_partials, const double* h_a = nullptr) {
   PK_REQUIRE(p.n >= 1 && p.n <= kMaxN, kErrLimit,
              "dimension " + std::to_string(p.n) + " exceeds the GPU kernel range n <= " +
                  std::to_string(kMaxN));
+  static_assert(sizeof(WalkArgs::col0) / sizeof(double) >= 2 * kMaxN, "col0 too small");
   F64Launch L{};
-  L.fn = tables().f64[cplx ? 1 : 0][p.n];
+  const bool c0p = B == 1 && h_a != nullptr && p.m >= 1;
+  L.fn = tables().f64[cplx ? 1 : 0][c0p ? 1 : 0][p.n];
   PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing fp64 kernel instantiation");
   L.per_warp = B > 1 ? 1 : 0;
   const int elem = cplx ? 16 : 8;
@@ -291,6 +297,12 @@ static F64Launch prepare_f64(DevCtx& c, const Plan& p, bool cplx, int algo, int 
   a.modp_out = nullptr;
   a.primes = nullptr;
   a.want_abs = want_abs ? 1 : 0;
+  if (c0p) {  // W[0] as stage_f64 builds it: Ryser a[:, 0], Glynn -2 a[1, :]
+    const int n = p.n, w = cplx ? 2 : 1;
+    for (int i = 0; i < n; ++i)
+      for (int z = 0; z < w; ++z)
+        a.col0[w * i + z] = algo == 0 ? h_a[w * (i * n) + z] : -2.0 * h_a[w * (n + i) + z];
+  }
   return L;
 }
 
@@ -514,7 +526,7 @@ static Node f64_range(const double* a, int n, bool cplx, int algo, uint64_t star
     if (t1 > t0) {
       auto* d_part = static_cast<double*>(c.partials.get((t1 - t0) * kPartialStride * 8));
       auto* d_out = static_cast<double*>(c.out.get(kPartialStride * 8));
-      F64Launch L = prepare_f64(c, p, cplx, algo, 1, d_a, t0, t1 - t0, want_abs, d_part);
+      F64Launch L = prepare_f64(c, p, cplx, algo, 1, d_a, t0, t1 - t0, want_abs, d_part, a);
       launch_walk(c, L.fn, L.grid, L.smem, L.args);
       auto* d_grp = static_cast<double*>(c.groups.get(group_scratch_doubles(1, t1 - t0, p.group) * 8));
       launch_reduce(c, d_part, 1, t0, t1 - t0, p.group, d_grp, d_out);
@@ -613,7 +625,8 @@ extern "C" int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex,
         const uint64_t nt = p.tiles_total;
         auto* d_part = static_cast<double*>(c.partials.get(nb * nt * kPartialStride * 8));
         auto* d_out = static_cast<double*>(c.out.get(nb * kPartialStride * 8));
-        F64Launch L = prepare_f64(c, p, cplx, algo, nb, d_a, 0, nt, abs_sums != nullptr, d_part);
+        F64Launch L = prepare_f64(c, p, cplx, algo, nb, d_a, 0, nt, abs_sums != nullptr, d_part,
+                                  a + b0 * mat);
         launch_walk(c, L.fn, L.grid, L.smem, L.args);
         auto* d_grp = static_cast<double*>(c.groups.get(group_scratch_doubles(nb, nt, p.group) * 8));
         launch_reduce(c, d_part, nb, 0, nt, p.group, d_grp, d_out);
@@ -754,9 +767,12 @@ struct ModpLaunch {
 // One launch per prime group: constants go into the kernel's grid-constant
 // parameter (args.mc); `group_primes` lists the group's moduli (the last `pf`
 // of them are fp64 primes of the hybrid kernel).
+// h_a: the caller's host residue matrices (P x n x n); walk column 0 of the
+// group's primes goes into the kernel parameter (WalkArgs::col0_modp).
 static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, const ModpGroup& G, int algo,
                                const void* d_a, const std::vector<uint64_t>& group_primes,
-                               uint64_t t0, uint64_t nt, unsigned long long* d_out) {
+                               uint64_t t0, uint64_t nt, unsigned long long* d_out,
+                               const uint64_t* h_a) {
   const bool lazy = G.lazy;
   const int pf = G.pf;
   PK_REQUIRE(p.n >= 1 && p.n <= kMaxN, kErrLimit,
@@ -812,6 +828,26 @@ static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, const ModpGroup& G, int
   for (int q = 0; q < pf; ++q) {
     a.mc.fp[q] = static_cast<double>(group_primes[pi + q]);
     a.mc.fpinv[q] = 1.0 / a.mc.fp[q];
+  }
+  if (!G.wide && !pf && p.m >= 1) {  // W2[dir][0] exactly as stage_modp builds it
+    static_assert(kCol0Stride >= kMaxN && kMaxP <= 4, "col0_modp too small");
+    const size_t nn = static_cast<size_t>(p.n) * p.n;
+    for (int q = 0; q < P; ++q) {
+      const uint32_t pq = static_cast<uint32_t>(group_primes[q]);
+      const uint64_t* aq = h_a + G.idx[q] * nn;
+      for (int i = 0; i < p.n; ++i) {
+        uint32_t v;
+        if (algo == 0) {
+          v = static_cast<uint32_t>(aq[i * p.n]);
+        } else {
+          uint32_t two = static_cast<uint32_t>(aq[p.n + i]) * 2u;
+          two = two >= pq ? two - pq : two;
+          v = two == 0 ? 0u : pq - two;
+        }
+        a.col0_modp[q * kCol0Stride + i] = v;
+        a.col0_modp[4 * kCol0Stride + q * kCol0Stride + i] = lazy ? 0u - v : (v == 0 ? 0u : pq - v);
+      }
+    }
   }
   return L;
 }
@@ -920,7 +956,7 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
         auto* d_o = static_cast<unsigned long long*>(c.modp_out.get(G.out_words() * 8));
         PK_CUDA(cudaMemcpyAsync(d_a, ha.data(), ha.size(), cudaMemcpyHostToDevice, c.stream));
         PK_CUDA(cudaMemsetAsync(d_o, 0, G.out_words() * 8, c.stream));
-        ModpLaunch L = prepare_modp(c, p, G, algo, d_a, gp, t0, t1 - t0, d_o);
+        ModpLaunch L = prepare_modp(c, p, G, algo, d_a, gp, t0, t1 - t0, d_o, a);
         launch_walk(c, L.fn, L.grid, L.smem, L.args);
         std::vector<unsigned long long> ho(G.out_words());
         PK_CUDA(cudaMemcpyAsync(ho.data(), d_o, ho.size() * 8, cudaMemcpyDeviceToHost, c.stream));
@@ -1024,7 +1060,7 @@ extern "C" int pk_job_f64_create(int device, const double* a, int n, int is_comp
     PK_CUDA(cudaMalloc(&j->d_out, kPartialStride * 8));
     PK_CUDA(cudaMalloc(&j->d_groups, group_scratch_doubles(1, j->nt, j->plan.group) * 8));
     F64Launch L = prepare_f64(c, j->plan, j->cplx, algo, 1, static_cast<double*>(j->d_a), j->t0,
-                              j->nt, false, j->d_part);
+                              j->nt, false, j->d_part, a);
     j->fn = L.fn;
     j->grid = L.grid;
     j->smem = L.smem;
@@ -1082,7 +1118,7 @@ extern "C" int pk_job_modp_create(int device, const uint64_t* a, const uint64_t*
       std::vector<uint64_t> gp;
       for (int k : G.idx) gp.push_back(primes[k]);
       ModpLaunch L = prepare_modp(c, j->plan, G, algo, static_cast<uint8_t*>(j->d_a) + a_off[gi],
-                                  gp, j->t0, j->nt, j->d_modp + o_off[gi]);
+                                  gp, j->t0, j->nt, j->d_modp + o_off[gi], a);
       j->groups.push_back(L);
       j->gdesc.push_back(G);
     }

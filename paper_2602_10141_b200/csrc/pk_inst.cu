@@ -2,7 +2,8 @@
 //
 // Compiled several times by the Makefile with different -D settings so the
 // ~200 kernels build in parallel:
-//   -DPK_INST_F64 -DPK_CPLX=0|1 -DPK_N_LO=.. -DPK_N_HI=..      fp64 real/complex
+//   -DPK_INST_F64 -DPK_CPLX=0|1 -DPK_C0P=0|1 -DPK_N_LO=.. -DPK_N_HI=..  fp64 real/complex,
+//                 column 0 from shared memory (batched) or the kernel parameter
 //   -DPK_INST_MODP -DPK_LAZY=0|1 -DPK_P=1..4 -DPK_N_LO=.. -DPK_N_HI=..  F_p, P primes per lane
 //   -DPK_INST_HYBRID -DPK_PI=1..2 -DPK_N_LO=.. -DPK_N_HI=..   F_p, PI Montgomery + 1 fp64 prime
 //   -DPK_INST_WIDE -DPK_P=1..2 -DPK_N_LO=.. -DPK_N_HI=..      F_p, wide moduli (Montgomery-64)
@@ -23,10 +24,12 @@ namespace pk {
 #if defined(PK_INST_F64)
 template <int... I>
 static void fill(const void** tbl, std::integer_sequence<int, I...>) {
-  ((tbl[PK_N_LO + I] = reinterpret_cast<const void*>(&walk_f64_kernel<PK_N_LO + I, (PK_CPLX != 0)>)),
+  ((tbl[PK_N_LO + I] = reinterpret_cast<const void*>(
+        &walk_f64_kernel<PK_N_LO + I, (PK_CPLX != 0), (PK_C0P != 0)>)),
    ...);
 }
-void PK_CAT(PK_CAT(PK_CAT(register_f64_c, PK_CPLX), _), PK_N_LO)(const void** tbl) {
+void PK_CAT(PK_CAT(PK_CAT(PK_CAT(PK_CAT(register_f64_c, PK_CPLX), _p), PK_C0P), _), PK_N_LO)(
+    const void** tbl) {
   fill(tbl, std::make_integer_sequence<int, PK_N_HI - PK_N_LO + 1>{});
 }
 #elif defined(PK_INST_MODP)

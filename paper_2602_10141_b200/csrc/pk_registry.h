@@ -9,9 +9,11 @@ constexpr int kMaxP = 4;   // primes per lane in the F_p kernel
 // N ranges compiled per object; must match the Makefile's INST_RANGES.
 #define PK_FOR_EACH_RANGE(X) X(1, 16) X(17, 28) X(29, 36) X(37, 42) X(43, 48)
 
-#define PK_DECL_F64(lo, hi)                      \
-  void register_f64_c0_##lo(const void** tbl); \
-  void register_f64_c1_##lo(const void** tbl);
+#define PK_DECL_F64(lo, hi)                         \
+  void register_f64_c0_p0_##lo(const void** tbl); \
+  void register_f64_c1_p0_##lo(const void** tbl); \
+  void register_f64_c0_p1_##lo(const void** tbl); \
+  void register_f64_c1_p1_##lo(const void** tbl);
 #define PK_DECL_MODP1(lazy, lo)                          \
   void register_modp_l##lazy##_p1_##lo(const void** tbl); \
   void register_modp_l##lazy##_p2_##lo(const void** tbl); \

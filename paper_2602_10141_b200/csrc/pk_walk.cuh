@@ -70,13 +70,18 @@ struct WalkArgs {
   const uint32_t* primes;        // F_p: [B][P]
   int want_abs;          // fp64: accumulate sum |term| (parity tolerance)
   ModConsts mc;          // F_p: constants of the (single) prime group of the launch
-#ifdef PK_EXP_CCOL0
-  double col0[2 * 48];   // micro-experiment: walk column 0 in the parameter space
-#endif
-#ifdef PK_EXP_CW
-  double cw[2 * 32 * 33];  // micro-experiment: the whole walk matrix (n = 32) in the parameter space
-#endif
+  // fp64, one matrix per launch (C0P kernels): walk column 0 (n values, complex
+  // interleaved), flipped on every odd step.  Read through the __grid_constant__
+  // parameter it compiles to uniform-register DFMA operands (LDCU): no shared
+  // load and no register-file read for half of all steps.
+  // F_p (walk_modp_kernel): the same column per prime and direction,
+  // [dir: plus, minus][prime q < 4][row i < 48], as stage_modp builds W2[dir][0].
+  union {
+    double col0[2 * 48];
+    uint32_t col0_modp[2 * 4 * 48];
+  };
 };
+constexpr int kCol0Stride = 48;  // rows per prime in WalkArgs::col0_modp
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
@@ -196,7 +201,11 @@ __device__ void stage_f64(typename F64T<CPLX>::T* sm, const double* a, int m, in
   }
 }
 
-template <int N, bool CPLX>
+// C0P: column 0 comes from the kernel parameter (WalkArgs::col0) instead of
+// shared memory; measured +6 % (complex) / +9 % (real) at n = 32
+// (profiles/r1_walk_experiments.txt).  Batched launches (a matrix per warp)
+// keep it in shared memory.
+template <int N, bool CPLX, bool C0P>
 struct F64Walker {
   using F = F64T<CPLX>;
   using T = typename F::T;
@@ -205,17 +214,11 @@ struct F64Walker {
   T r[N];
   double s_re, c_re, s_im, c_im, abs_acc;
   bool want_abs;
-#ifdef PK_EXP_CCOL0
-  const T* c0;  // column 0 in the __grid_constant__ parameter (constant-bank operands)
-#endif
-#ifdef PK_EXP_CW
-  const T* cw;  // all columns in the __grid_constant__ parameter
-#endif
+  const T* c0;  // C0P: column 0 in the __grid_constant__ parameter
 
   // Product of the state as a binary tree evaluated depth-first (a binary
   // counter over the leaves): the same N - 1 multiplies as a chain, depth
   // ~log2 N, and at most log2 N + 1 partial products live at once.
-#ifndef PK_EXP_TREE2
   __device__ __forceinline__ T tree() const {
     constexpr int LOG = 7;
     T st[LOG];
@@ -246,44 +249,6 @@ struct F64Walker {
     }
     return acc;
   }
-#endif
-
-#ifdef PK_EXP_TREE2  // micro-experiments only: two interleaved half trees
-  __device__ __forceinline__ T tree() const {
-    constexpr int H = N / 2, LOG = 7;
-    T sa[LOG], sb[LOG];
-#pragma unroll
-    for (int j = 0; j < H; ++j) {
-      T va = r[j], vb = r[H + j];
-      int l = 0;
-#pragma unroll
-      for (; l < LOG && ((j >> l) & 1); ++l) {
-        mul_acc(sa[l], va);
-        mul_acc(sb[l], vb);
-        va = sa[l];
-        vb = sb[l];
-      }
-      sa[l] = va;
-      sb[l] = vb;
-    }
-    T acc = r[0];
-    bool have = false;
-#pragma unroll
-    for (int l = 0; l < LOG; ++l) {
-      if ((H >> l) & 1) {
-        mul_acc(sa[l], sb[l]);
-        if (have) {
-          mul_acc(acc, sa[l]);
-        } else {
-          acc = sa[l];
-          have = true;
-        }
-      }
-    }
-    if constexpr (N & 1) mul_acc(acc, r[N - 1]);
-    return acc;
-  }
-#endif
 
   // flip one column with direction sg and return the new term's product
   __device__ __forceinline__ T step(const T* __restrict__ col, double sg) {
@@ -353,23 +318,13 @@ struct F64Walker {
       const T po = step(W, StepPlan::minus_odd(1, k, lane_minus) ? -1.0 : 1.0);
       add_pair(pe, po);
     }
-#ifdef PK_EXP_UNROLL
-#pragma unroll 2
-#endif
     for (uint32_t e = 2; e < L; e += 2) {
       const int b = __ffs(e) - 1;
-#ifdef PK_EXP_CW
-      const T pe = step(cw + b * NS, StepPlan::minus_even(e, k, lane_minus) ? -1.0 : 1.0);
-#else
       const T pe = step(W + b * NS, StepPlan::minus_even(e, k, lane_minus) ? -1.0 : 1.0);
-#endif
-      // (e >> 31) is always 0: it keeps column 0 from being hoisted out of
-      // the loop into registers (which would spill the state)
-#ifdef PK_EXP_CCOL0
-      const T po = step(c0, StepPlan::minus_odd(e + 1, k, lane_minus) ? -1.0 : 1.0);
-#else
-      const T po = step(W + (e >> 31) * NS, StepPlan::minus_odd(e + 1, k, lane_minus) ? -1.0 : 1.0);
-#endif
+      // shared-memory column 0: (e >> 31) is always 0; it keeps the column
+      // from being hoisted out of the loop into registers (spilling the state)
+      const T* c = C0P ? c0 : W + (e >> 31) * NS;
+      const T po = step(c, StepPlan::minus_odd(e + 1, k, lane_minus) ? -1.0 : 1.0);
       add_pair(pe, po);
     }
   }
@@ -398,10 +353,10 @@ __device__ __forceinline__ double warp_sum_tree(double v) {
   return v;
 }
 
-template <int N, bool CPLX>
+template <int N, bool CPLX, bool C0P>
 __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
     walk_f64_kernel(const __grid_constant__ WalkArgs args) {
-  using W_ = F64Walker<N, CPLX>;
+  using W_ = F64Walker<N, CPLX, C0P>;
   using T = typename W_::T;
   constexpr int NS = W_::NS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -425,12 +380,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
   }
   W_ w;
   w.want_abs = args.want_abs != 0;
-#ifdef PK_EXP_CCOL0
-  w.c0 = reinterpret_cast<const T*>(args.col0);
-#endif
-#ifdef PK_EXP_CW
-  w.cw = reinterpret_cast<const T*>(args.cw);
-#endif
+  w.c0 = C0P ? reinterpret_cast<const T*>(args.col0) : nullptr;
   // Ryser's global sign (-1)^n: the term sign at a segment start (its Gray
   // code has even popcount).  Negation is exact and commutes with the TwoSum
   // tree, so it is applied per lane.
@@ -533,6 +483,7 @@ struct ModpWalker {
   uint32_t r[P][N];
   const ModConsts* mc;              // p, -1/p, kneg (multiple of p bounding every REDC output)
   unsigned long long acc[P];        // even steps add y, odd steps kneg - y
+  const uint32_t* c0;               // column 0, both directions, in the kernel parameter
 
   __device__ __forceinline__ uint32_t p(int q) const { return mc->p[q]; }
 
@@ -609,6 +560,24 @@ struct ModpWalker {
       acc[q] += static_cast<unsigned long long>(ye[q]) + (mc->kneg[q] - yo[q]);
   }
 
+  // odd step (column 0) from the parameter copy (lazy rows): the direction is
+  // warp-uniform, so each branch adds a fixed parameter array (uniform-register
+  // IADD3 operands, no shared load)
+  __device__ __forceinline__ void step_c0(bool minus, uint32_t* y) {
+    if (minus) {
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int j = 0; j < N; ++j) upd(r[q][j], c0[4 * kCol0Stride + q * kCol0Stride + j], p(q));
+    } else {
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+#pragma unroll
+        for (int j = 0; j < N; ++j) upd(r[q][j], c0[q * kCol0Stride + j], p(q));
+    }
+    tree(y);
+  }
+
   __device__ __forceinline__ void walk(const uint32_t* __restrict__ W2,
                                        const uint32_t* __restrict__ base, int m, int k,
                                        uint64_t seg) {
@@ -639,8 +608,14 @@ struct ModpWalker {
     for (uint32_t e = 2; e < L; e += 2) {
       const int b = __ffs(e) - 1;
       step((StepPlan::minus_even(e, k, lane_minus) ? Wm : W2) + b * CS, ye);
-      // (e >> 31) is always 0: keeps column 0 from being hoisted into registers
-      step((StepPlan::minus_odd(e + 1, k, lane_minus) ? Wm : W2) + (e >> 31) * CS, yo);
+      if constexpr (LAZY) {
+        step_c0(StepPlan::minus_odd(e + 1, k, lane_minus), yo);
+      } else {
+        // reduced rows keep column 0 in shared memory: with parameter operands
+        // ptxas hoists the loop-invariant (c - p) of min(v, v - p) and spills.
+        // (e >> 31) is always 0: it keeps the column from being hoisted too.
+        step((StepPlan::minus_odd(e + 1, k, lane_minus) ? Wm : W2) + (e >> 31) * CS, yo);
+      }
       add_pair(ye, yo);
     }
   }
@@ -662,6 +637,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * P))
   __syncthreads();
   W_ w;
   w.mc = &args.mc;
+  w.c0 = args.col0_modp;
   unsigned long long tot[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) tot[q] = 0;

@@ -1,5 +1,6 @@
-// Micro-experiment harness: time walk_f64_kernel<N, complex> under compile-time
-// variants (-DPK_EXP_NOKAHAN, -DPK_EXP_NOLDS, -DPK_MINCTA_T=...).
+// Micro-experiment harness: time walk_f64_kernel<N, complex, C0P> under compile-time
+// variants (-DPK_EXP_NOKAHAN, -DPK_EXP_NOLDS, -DPK_MINCTA_T=..., -DPK_EXP_SMEM_C0 for
+// column 0 from shared memory instead of the kernel parameter).
 //   nvcc -O3 -std=c++17 -arch=sm_100a -I../../paper_2602_10141_b200/csrc walk_exp.cu
 #include <cstdio>
 #include <vector>
@@ -23,7 +24,12 @@ int main(int argc, char** argv) {
   cudaMemcpy(da, a.data(), a.size() * 8, cudaMemcpyHostToDevice);
   const uint64_t tiles = 1ull << (m - k - 5);
   cudaMalloc(&dp, tiles * 5 * 8);
-  const void* fn = (const void*)&walk_f64_kernel<N, CPLX>;
+#ifdef PK_EXP_SMEM_C0
+  constexpr bool C0P = false;
+#else
+  constexpr bool C0P = true;
+#endif
+  const void* fn = (const void*)&walk_f64_kernel<N, CPLX, C0P>;
   const int eb = CPLX ? 16 : 8;
   const int smem = (m + 1) * col_stride(n, eb) * eb;
   int occ = 0, sms = 0;
@@ -34,18 +40,10 @@ int main(int argc, char** argv) {
   WalkArgs w{};
   w.a = da; w.B = 1; w.n = n; w.m = m; w.algo = 0; w.k = k; w.per_warp_slot = 0;
   w.tile0 = 0; w.tiles = tiles; w.segs_total = 1ull << (m - k); w.partials = dp; w.want_abs = 0;
-#ifdef PK_EXP_CW
-  for (int b = 0; b < n; ++b)
-    for (int i = 0; i < n; ++i) {  // Ryser W[b][i] = a[i][b]
-      if (CPLX) { w.cw[2 * (b * 32 + i)] = a[2 * (i * n + b)]; w.cw[2 * (b * 32 + i) + 1] = a[2 * (i * n + b) + 1]; }
-    }
-#endif
-#ifdef PK_EXP_CCOL0
   for (int i = 0; i < n; ++i) {  // Ryser column 0 = a[:, 0]
     if (CPLX) { w.col0[2 * i] = a[2 * (i * n)]; w.col0[2 * i + 1] = a[2 * (i * n) + 1]; }
     else w.col0[i] = a[i * n];
   }
-#endif
   const int grid = sms * occ;
   void* args[] = {&w};
   cudaLaunchKernel(fn, grid, kWalkThreads, args, smem, 0);
