@@ -767,12 +767,9 @@ struct ModpLaunch {
 // One launch per prime group: constants go into the kernel's grid-constant
 // parameter (args.mc); `group_primes` lists the group's moduli (the last `pf`
 // of them are fp64 primes of the hybrid kernel).
-// h_a: the caller's host residue matrices (P x n x n); walk column 0 of the
-// group's primes goes into the kernel parameter (WalkArgs::col0_modp).
 static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, const ModpGroup& G, int algo,
                                const void* d_a, const std::vector<uint64_t>& group_primes,
-                               uint64_t t0, uint64_t nt, unsigned long long* d_out,
-                               const uint64_t* h_a) {
+                               uint64_t t0, uint64_t nt, unsigned long long* d_out) {
   const bool lazy = G.lazy;
   const int pf = G.pf;
   PK_REQUIRE(p.n >= 1 && p.n <= kMaxN, kErrLimit,
@@ -828,26 +825,6 @@ static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, const ModpGroup& G, int
   for (int q = 0; q < pf; ++q) {
     a.mc.fp[q] = static_cast<double>(group_primes[pi + q]);
     a.mc.fpinv[q] = 1.0 / a.mc.fp[q];
-  }
-  if (!G.wide && !pf && p.m >= 1) {  // W2[dir][0] exactly as stage_modp builds it
-    static_assert(kCol0Stride >= kMaxN && kMaxP <= 4, "col0_modp too small");
-    const size_t nn = static_cast<size_t>(p.n) * p.n;
-    for (int q = 0; q < P; ++q) {
-      const uint32_t pq = static_cast<uint32_t>(group_primes[q]);
-      const uint64_t* aq = h_a + G.idx[q] * nn;
-      for (int i = 0; i < p.n; ++i) {
-        uint32_t v;
-        if (algo == 0) {
-          v = static_cast<uint32_t>(aq[i * p.n]);
-        } else {
-          uint32_t two = static_cast<uint32_t>(aq[p.n + i]) * 2u;
-          two = two >= pq ? two - pq : two;
-          v = two == 0 ? 0u : pq - two;
-        }
-        a.col0_modp[q * kCol0Stride + i] = v;
-        a.col0_modp[4 * kCol0Stride + q * kCol0Stride + i] = lazy ? 0u - v : (v == 0 ? 0u : pq - v);
-      }
-    }
   }
   return L;
 }
@@ -956,7 +933,7 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
         auto* d_o = static_cast<unsigned long long*>(c.modp_out.get(G.out_words() * 8));
         PK_CUDA(cudaMemcpyAsync(d_a, ha.data(), ha.size(), cudaMemcpyHostToDevice, c.stream));
         PK_CUDA(cudaMemsetAsync(d_o, 0, G.out_words() * 8, c.stream));
-        ModpLaunch L = prepare_modp(c, p, G, algo, d_a, gp, t0, t1 - t0, d_o, a);
+        ModpLaunch L = prepare_modp(c, p, G, algo, d_a, gp, t0, t1 - t0, d_o);
         launch_walk(c, L.fn, L.grid, L.smem, L.args);
         std::vector<unsigned long long> ho(G.out_words());
         PK_CUDA(cudaMemcpyAsync(ho.data(), d_o, ho.size() * 8, cudaMemcpyDeviceToHost, c.stream));
@@ -1118,7 +1095,7 @@ extern "C" int pk_job_modp_create(int device, const uint64_t* a, const uint64_t*
       std::vector<uint64_t> gp;
       for (int k : G.idx) gp.push_back(primes[k]);
       ModpLaunch L = prepare_modp(c, j->plan, G, algo, static_cast<uint8_t*>(j->d_a) + a_off[gi],
-                                  gp, j->t0, j->nt, j->d_modp + o_off[gi], a);
+                                  gp, j->t0, j->nt, j->d_modp + o_off[gi]);
       j->groups.push_back(L);
       j->gdesc.push_back(G);
     }

@@ -74,14 +74,10 @@ struct WalkArgs {
   // interleaved), flipped on every odd step.  Read through the __grid_constant__
   // parameter it compiles to uniform-register DFMA operands (LDCU): no shared
   // load and no register-file read for half of all steps.
-  // F_p (walk_modp_kernel): the same column per prime and direction,
-  // [dir: plus, minus][prime q < 4][row i < 48], as stage_modp builds W2[dir][0].
-  union {
-    double col0[2 * 48];
-    uint32_t col0_modp[2 * 4 * 48];
-  };
+  // (F_p kernels keep column 0 in shared memory: with parameter operands the
+  // lazy walk measured 8-10 % slower, profiles/r1_modp_rates_c0.json.)
+  double col0[2 * 48];
 };
-constexpr int kCol0Stride = 48;  // rows per prime in WalkArgs::col0_modp
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
@@ -483,7 +479,6 @@ struct ModpWalker {
   uint32_t r[P][N];
   const ModConsts* mc;              // p, -1/p, kneg (multiple of p bounding every REDC output)
   unsigned long long acc[P];        // even steps add y, odd steps kneg - y
-  const uint32_t* c0;               // column 0, both directions, in the kernel parameter
 
   __device__ __forceinline__ uint32_t p(int q) const { return mc->p[q]; }
 
@@ -560,24 +555,6 @@ struct ModpWalker {
       acc[q] += static_cast<unsigned long long>(ye[q]) + (mc->kneg[q] - yo[q]);
   }
 
-  // odd step (column 0) from the parameter copy (lazy rows): the direction is
-  // warp-uniform, so each branch adds a fixed parameter array (uniform-register
-  // IADD3 operands, no shared load)
-  __device__ __forceinline__ void step_c0(bool minus, uint32_t* y) {
-    if (minus) {
-#pragma unroll
-      for (int q = 0; q < P; ++q)
-#pragma unroll
-        for (int j = 0; j < N; ++j) upd(r[q][j], c0[4 * kCol0Stride + q * kCol0Stride + j], p(q));
-    } else {
-#pragma unroll
-      for (int q = 0; q < P; ++q)
-#pragma unroll
-        for (int j = 0; j < N; ++j) upd(r[q][j], c0[q * kCol0Stride + j], p(q));
-    }
-    tree(y);
-  }
-
   __device__ __forceinline__ void walk(const uint32_t* __restrict__ W2,
                                        const uint32_t* __restrict__ base, int m, int k,
                                        uint64_t seg) {
@@ -608,14 +585,8 @@ struct ModpWalker {
     for (uint32_t e = 2; e < L; e += 2) {
       const int b = __ffs(e) - 1;
       step((StepPlan::minus_even(e, k, lane_minus) ? Wm : W2) + b * CS, ye);
-      if constexpr (LAZY) {
-        step_c0(StepPlan::minus_odd(e + 1, k, lane_minus), yo);
-      } else {
-        // reduced rows keep column 0 in shared memory: with parameter operands
-        // ptxas hoists the loop-invariant (c - p) of min(v, v - p) and spills.
-        // (e >> 31) is always 0: it keeps the column from being hoisted too.
-        step((StepPlan::minus_odd(e + 1, k, lane_minus) ? Wm : W2) + (e >> 31) * CS, yo);
-      }
+      // (e >> 31) is always 0: keeps column 0 from being hoisted into registers
+      step((StepPlan::minus_odd(e + 1, k, lane_minus) ? Wm : W2) + (e >> 31) * CS, yo);
       add_pair(ye, yo);
     }
   }
@@ -637,7 +608,6 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * P))
   __syncthreads();
   W_ w;
   w.mc = &args.mc;
-  w.c0 = args.col0_modp;
   unsigned long long tot[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) tot[q] = 0;

@@ -1,4 +1,5 @@
-"""Run one resident walk for profiling:  python tools/prof_one.py {f64c|f64r|modp|modpr} N [iters]"""
+"""Run one resident walk for profiling:
+    python tools/prof_one.py {f64c|f64r|modp|modpr|hyb|basis|wide|batch|batchr} N [iters]"""
 import os
 import sys
 
@@ -27,13 +28,18 @@ if kind.startswith("f64"):
     q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
     a = q if kind == "f64c" else q.real.copy()
     job = nat.Job.f64(a, "ryser", 0, 1 << n)
+elif kind in ("basis", "wide"):
+    from paper_2602_10141_b200 import modular
+    ps = (list(modular.gpu_prime_basis(n).primes) if kind == "basis"
+          else list(modular.find_primes(n, max_bits=59).primes[:1]))
+    job = nat.Job.modp(np.stack([schur_res(n, p) for p in ps]), ps, "ryser", 0, 1 << n)
 elif kind == "hyb":
     from paper_2602_10141_b200 import modular
-    ps = list(modular.gpu_prime_basis(n, needed_product_bits=90).primes)[:4]
+    ps = modular.prime_pool(n, "lazy", 2) + modular.prime_pool(n, "fp64", 2)  # two hybrid pairs
     job = nat.Job.modp(np.stack([schur_res(n, p) for p in ps]), ps, "ryser", 0, 1 << n)
 else:
     below = (1 << 31) // n if kind == "modp" else (1 << 31)
     ps = primes_1modn(n, below, 4)
     job = nat.Job.modp(np.stack([schur_res(n, p) for p in ps]), ps, "ryser", 0, 1 << n)
 tot, walk, res = job.run(iters)
-print(kind, n, job.info(), f"walk {walk / iters:.3f} ms", f"{iters * n * 2.0 ** n * (4 if ('modp' in kind or kind == 'hyb') else 1) / (walk / 1e3):.3e} upd/s")
+print(kind, n, job.info(), f"walk {walk / iters:.3f} ms", f"{iters * n * 2.0 ** n * (len(ps) if kind.startswith(('modp', 'hyb', 'basis', 'wide')) else 1) / (walk / 1e3):.3e} upd/s")
