@@ -101,8 +101,11 @@ int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex, int algo, 
  *   out[k] = exact signed walk sum over the range mod primes[k], in [0, p):
  *            the value sum(kernels.ryser_partial_modp(a_k, blk...)) mod p
  *            (kernels.py:250-290, 433-434); Glynn is NOT scaled by 2^(1-n).
- * Odd p < 2^31 run in the Montgomery-32 production kernel with up to four
- * primes per lane; other moduli use the generic 64-bit walker.
+ * Odd p < 2^31 run in the Montgomery-32 kernels (up to four primes per lane;
+ * fp64-eligible primes pair with a Montgomery prime in the hybrid kernel);
+ * odd 2^31 <= p < 2^62 run in the Montgomery-64 kernel (two per lane for
+ * n <= 36); even moduli, and the ragged ends of unaligned ranges, use the
+ * per-block parity walker.
  */
 int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, int n, int algo,
                   uint64_t start, uint64_t length, int ndev, uint64_t* out);
@@ -116,6 +119,7 @@ typedef struct pk_job pk_job;
 
 int pk_job_f64_create(int device, const double* a, int n, int is_complex, int algo,
                       uint64_t start, uint64_t length, pk_job** job);
+/* F_p jobs take odd moduli p < 2^62 (every prime of the fast kernels). */
 int pk_job_modp_create(int device, const uint64_t* a, const uint64_t* primes, int P, int n,
                        int algo, uint64_t start, uint64_t length, pk_job** job);
 /*

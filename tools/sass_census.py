@@ -12,10 +12,13 @@ import sys
 
 LIB = "paper_2602_10141_b200/_lib/libpermkit_gpu.so"
 KERNELS = [
-    ("walk_f64_kernel<32, true>", r"_ZN2pk15walk_f64_kernelILi32ELb1EEEvNS_8WalkArgsE"),
-    ("walk_f64_kernel<32, false>", r"_ZN2pk15walk_f64_kernelILi32ELb0EEEvNS_8WalkArgsE"),
+    ("walk_f64_kernel<32, complex, col0 in param>", r"_ZN2pk15walk_f64_kernelILi32ELb1ELb1EEEvNS_8WalkArgsE"),
+    ("walk_f64_kernel<32, real, col0 in param>", r"_ZN2pk15walk_f64_kernelILi32ELb0ELb1EEEvNS_8WalkArgsE"),
+    ("walk_f64_kernel<23, complex, batched>", r"_ZN2pk15walk_f64_kernelILi23ELb1ELb0EEEvNS_8WalkArgsE"),
+    ("walk_modp_kernel<36, 3, reduced>", r"_ZN2pk16walk_modp_kernelILi36ELi3ELb0EEEvNS_8WalkArgsE"),
     ("walk_modp_kernel<36, 4, lazy>", r"_ZN2pk16walk_modp_kernelILi36ELi4ELb1EEEvNS_8WalkArgsE"),
-    ("walk_modp_kernel<32, 4, reduced>", r"_ZN2pk16walk_modp_kernelILi32ELi4ELb0EEEvNS_8WalkArgsE"),
+    ("walk_hybrid_kernel<36, 1, 1>", r"_ZN2pk18walk_hybrid_kernelILi36ELi1ELi1EEEvNS_8WalkArgsE"),
+    ("walk_modp64_kernel<32, 1>", r"_ZN2pk18walk_modp64_kernelILi32ELi1EEEvNS_8WalkArgsE"),
 ]
 
 
