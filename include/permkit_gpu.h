@@ -103,8 +103,8 @@ int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex, int algo, 
  *            (kernels.py:250-290, 433-434); Glynn is NOT scaled by 2^(1-n).
  * Odd p < 2^31 run in the Montgomery-32 kernels (up to four primes per lane;
  * fp64-eligible primes pair with a Montgomery prime in the hybrid kernel);
- * odd 2^31 <= p < 2^62 run in the Montgomery-64 kernel (two per lane for
- * n <= 36); even moduli, and the ragged ends of unaligned ranges, use the
+ * odd 2^31 <= p < 2^62 run in the Montgomery-64 kernel (one per lane);
+ * even moduli, and the ragged ends of unaligned ranges, use the
  * per-block parity walker.
  */
 int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, int n, int algo,

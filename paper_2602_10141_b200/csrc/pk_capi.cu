@@ -77,11 +77,8 @@ static const Tables& tables() {
     PK_FOR_EACH_HYBRID_RANGE(PK_REGH)
 #undef PK_REGH
 #define PK_REGW1(lo, hi) register_wide_p1_##lo(t.wide[1]);
-#define PK_REGW2(lo, hi) register_wide_p2_##lo(t.wide[2]);
     PK_FOR_EACH_RANGE(PK_REGW1)
-    PK_FOR_EACH_WIDE2_RANGE(PK_REGW2)
 #undef PK_REGW1
-#undef PK_REGW2
     return t;
   }();
   return t;
@@ -872,7 +869,7 @@ static std::vector<ModpGroup> group_primes(const std::vector<int>& fast, const u
       i += P;
     }
   }
-  const int wmax = n <= kWide2MaxN ? kMaxPWide : 1;
+  const int wmax = kMaxPWide;
   for (size_t i = 0; i < wd.size();) {
     const int P = static_cast<int>(std::min<size_t>(wmax, wd.size() - i));
     ModpGroup g{P, false, 0, {}, true};

@@ -28,17 +28,12 @@ constexpr int kHybridMinN = 17;
   void register_hybrid_pi2_##lo(const void** tbl);
 PK_FOR_EACH_HYBRID_RANGE(PK_DECL_HYBRID)
 #undef PK_DECL_HYBRID
-// wide (2^31 <= p < 2^62, Montgomery-64) kernels: one prime per lane for every
-// N, two for N <= kWide2MaxN
-constexpr int kMaxPWide = 2;
-constexpr int kWide2MaxN = 36;
-#define PK_FOR_EACH_WIDE2_RANGE(X) X(1, 16) X(17, 28) X(29, 36)
+// wide (2^31 <= p < 2^62, Montgomery-64) kernels: one prime per lane (two per
+// lane measured 20-30 % slower per prime: register pressure, profiles/r1_modp_rates_wide2.json)
+constexpr int kMaxPWide = 1;
 #define PK_DECL_WIDE1(lo, hi) void register_wide_p1_##lo(const void** tbl);
-#define PK_DECL_WIDE2(lo, hi) void register_wide_p2_##lo(const void** tbl);
 PK_FOR_EACH_RANGE(PK_DECL_WIDE1)
-PK_FOR_EACH_WIDE2_RANGE(PK_DECL_WIDE2)
 #undef PK_DECL_WIDE1
-#undef PK_DECL_WIDE2
 PK_FOR_EACH_RANGE(PK_DECL_F64)
 PK_FOR_EACH_RANGE(PK_DECL_MODP)
 #undef PK_DECL_F64

@@ -213,15 +213,32 @@ struct Modp64Walker {
     for (int q = 0; q < P; ++q) acc_lo[q] = acc_hi[q] = 0ull;
     const uint32_t L = 1u << k;
     const bool lane_minus = seg & 1;
-    uint64_t ye[P], yo[P];
-    tree(ye);
-    step(StepPlan::minus_odd(1, k, lane_minus) ? Wm : W2, yo);
-    add_pair(ye, yo);
-    for (uint32_t e = 2; e < L; e += 2) {
-      const int b = __ffs(e) - 1;
-      step((StepPlan::minus_even(e, k, lane_minus) ? Wm : W2) + b * CS, ye);
-      step((StepPlan::minus_odd(e + 1, k, lane_minus) ? Wm : W2) + (e >> 31) * CS, yo);
-      add_pair(ye, yo);
+    // One step (one product tree) per iteration: a REDC-64 tree is ~1,200
+    // instructions, and the two-step body of the 32-bit walk overflowed the
+    // instruction cache here (ncu: 2.1 no_instruction stalls per issue).
+    uint64_t y[P], ye[P];
+    for (uint32_t s = 0; s < L; ++s) {
+      if (s) {
+        const int b = __ffs(s) - 1;
+        const bool minus = (b == k - 1) ? lane_minus : ((s >> (b + 1)) & 1);
+        const uint64_t* col = (minus ? Wm : W2) + b * CS;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+#pragma unroll
+          for (int j = 0; j < NS; j += 2) {
+            const ulonglong2 c = *reinterpret_cast<const ulonglong2*>(col + q * NS + j);
+            upd(r[q][j], c.x, p(q));
+            if (j + 1 < N) upd(r[q][j + 1], c.y, p(q));
+          }
+        }
+      }
+      tree(y);
+      if (s & 1) {
+        add_pair(ye, y);
+      } else {
+#pragma unroll
+        for (int q = 0; q < P; ++q) ye[q] = y[q];
+      }
     }
   }
 };

@@ -384,7 +384,7 @@ def _wide_moduli(n):
 
 @pytest.mark.parametrize("n", [13, 24, 30, 33, 36])
 def test_wide_moduli_vs_oracle(gpu, n):
-    """Montgomery-64 walk (2^31 <= p < 2^62, two moduli per lane when n <= 36)."""
+    """Montgomery-64 walk (2^31 <= p < 2^62, one modulus per lane, three launches)."""
     rng = np.random.default_rng(100 + n)
     mods = _wide_moduli(n)
     mats = np.stack([rng.integers(0, p, size=(n, n), dtype=np.uint64) for p in mods])
