@@ -320,11 +320,12 @@ def secondary(args, nat, modular):
                              / (walk / 1e3),
                              "walk_ms": walk / 2, **job.info()}
     job.close()
-    # C2-style batched sampler (ensembles.sample_permanents): host sampling overlapped
-    # with the batched GPU walk; a 2,000-sample slice of the 50,000-sample config
+    # C2-style batched sampler (ensembles.sample_permanents): host sampling (a process
+    # pool) overlapped with the batched GPU walk; an 8,192-sample slice (two chunks) of
+    # the 50,000-sample config.  The warm-up call starts the sampler's process pool.
     from paper_2602_10141_b200 import ensembles
-    spec = ensembles.EnsembleSpec("haar-u", 23, 2000, SEED)
-    ensembles.sample_permanents(ensembles.EnsembleSpec("haar-u", 23, 64, SEED))
+    spec = ensembles.EnsembleSpec("haar-u", 23, 8192, SEED)
+    ensembles.sample_permanents(ensembles.EnsembleSpec("haar-u", 23, 1024, SEED))
     t0 = time.perf_counter()
     vals = ensembles.sample_permanents(spec)
     dt = time.perf_counter() - t0

@@ -237,6 +237,15 @@ def test_sample_batch_thread_invariant():
         ensembles.sample_gue(ensembles.EnsembleSpec("goe", 3, 1, 0))
 
 
+def test_sample_batch_process_pool_bit_identical():
+    """Large batches go through the spawn process pool; same bytes as one process."""
+    for kind in ("haar-u", "goe"):
+        spec = ensembles.EnsembleSpec(kind, 7, 700, 2602)
+        a = ensembles.sample_batch(spec, 5, 705, threads=1)
+        b = ensembles.sample_batch(spec, 5, 705, threads=3)
+        assert a.shape == (700, 7, 7) and a.tobytes() == b.tobytes()
+
+
 # --------------------------------------------------------------------------- geodesics / matrices
 
 def test_geodesic_matrices_match_reference():
