@@ -411,6 +411,30 @@ def test_wide_moduli_vs_oracle(gpu, n):
             assert got2[0] == want(0, algo, st2, ln2), (n, algo, "unaligned")
 
 
+def test_resident_jobs_match_one_shot_calls(gpu):
+    """bench.py's device-resident jobs return what the one-shot C ABI returns: an F_p
+    job mixing every launch-group kind (reduced, lazy, hybrid, wide) and an fp64 job."""
+    from paper_2602_10141_b200 import _native as nat
+    n = 24
+    ps = (modular.prime_pool(n, "reduced", 2) + modular.prime_pool(n, "lazy", 2)
+          + modular.prime_pool(n, "fp64", 1) + list(modular.find_primes(n, max_bits=59).primes[:1]))
+    mats = np.stack([modular._root_matrix_u64(n, p, modular.primitive_nth_root(p, n)) for p in ps])
+    for algo in ("ryser", "glynn"):
+        m = n if algo == "ryser" else n - 1
+        want = gpu.ryser_modp(mats, ps, algo, 0, 1 << m)
+        job = nat.Job.modp(mats, ps, algo, 0, 1 << m)
+        _, _, got = job.run(2)
+        assert job.info()["launches"] == 4  # reduced x2, hybrid (lazy + fp64), lazy x1, wide
+        job.close()
+        assert [int(x) for x in got] == want, algo
+    a = ensembles.sample_matrix("haar-u", 20, 2602, 3)
+    job = nat.Job.f64(a, "ryser", 0, 1 << 20)
+    _, _, root = job.run(3)  # (s_re, c_re, s_im, c_im, abs) of the last run
+    job.close()
+    s1, c1, _ = nat.ryser_f64(a, "ryser", 0, 1 << 20, 1)
+    assert complex(root[0], root[2]) == s1 and complex(root[1], root[3]) == c1
+
+
 def test_schur_default_59bit_basis_through_wide_kernel(gpu):
     """The reference's default basis (59-bit) at n = 23, 25 against SURVEY Appendix A."""
     v23, b23, w23 = modular.schur_permanent_exact(23)
