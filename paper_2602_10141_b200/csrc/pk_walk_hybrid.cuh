@@ -23,6 +23,9 @@
 
 #include "pk_walk.cuh"
 
+#ifndef PK_HYB_MINCTA
+#define PK_HYB_MINCTA 2
+#endif
 namespace pk {
 
 __host__ __device__ constexpr bool fp64_prime_ok(uint64_t p, int n) {
@@ -202,7 +205,7 @@ struct HybridWalker {
 // One (Montgomery + fp64) prime group per launch (args.B == 1, constants in args.mc;
 // the residue matrices of the PI Montgomery primes come first, then the fp64 ones).
 template <int N, int PI, int PF>
-__global__ void __launch_bounds__(kWalkThreads, 2)
+__global__ void __launch_bounds__(kWalkThreads, PK_HYB_MINCTA)
     walk_hybrid_kernel(const __grid_constant__ WalkArgs args) {
   constexpr int P = PI + PF;
   constexpr int NS4 = col_stride(N, 4);
