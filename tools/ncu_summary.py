@@ -53,10 +53,8 @@ def main(rep):
     print(f"-- instruction mix (warp-level, total {tot:.3e})")
     for op, c in ops.most_common(16):
         print(f"   {op:22s} {c:14d} {c / tot:6.3f}")
-
-
-if __name__ == "__main__":
-    main(sys.argv[1])
+    print("-- stall samples by opcode (share; top reasons)")
+    stalls_by_op(rep)
 
 
 def stalls_by_op(rep, top=12):
@@ -76,3 +74,7 @@ def stalls_by_op(rep, top=12):
     for op, v in sorted(agg.items(), key=lambda kv: -sum(kv[1].values()))[:top]:
         s = sum(v.values())
         print(f"   {op:16s} {s / tot:6.3f}  " + " ".join(f"{c[6:]}={n / s:.2f}" for c, n in v.most_common(4)))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
