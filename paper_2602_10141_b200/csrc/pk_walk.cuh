@@ -248,6 +248,11 @@ struct F64Walker {
 
   // flip one column with direction sg and return the new term's product
   __device__ __forceinline__ T step(const T* __restrict__ col, double sg) {
+    update(col, sg);
+    return tree();
+  }
+
+  __device__ __forceinline__ void update(const T* __restrict__ col, double sg) {
     if constexpr (CPLX) {
 #pragma unroll
       for (int j = 0; j < N; ++j) {
@@ -266,7 +271,6 @@ struct F64Walker {
       }
       if constexpr (N & 1) fma_upd(r[N - 1], sg, col[N - 1]);
     }
-    return tree();
   }
 
   // Terms of a step pair (even e, odd e+1) carry opposite signs: their
