@@ -49,7 +49,7 @@ const char* last_error_cstr() { return g_last_error.c_str(); }
 struct Tables {
   const void* f64[2][2][kMaxN + 1] = {};          // [cplx][column 0 in param][N]
   const void* modp[2][kMaxP + 1][kMaxN + 1] = {};  // [lazy][P][N]
-  const void* hybrid[3][kMaxN + 1] = {};            // [PI][N], one fp64 prime
+  const void* hybrid[2][3][kMaxN + 1] = {};         // [wide fp][PI][N], one fp64 prime
   const void* wide[kMaxPWide + 1][kMaxN + 1] = {};  // [P][N], Montgomery-64
 };
 
@@ -71,9 +71,11 @@ static const Tables& tables() {
   register_modp_l1_p4_##lo(t.modp[1][4]);
     PK_FOR_EACH_RANGE(PK_REG)
 #undef PK_REG
-#define PK_REGH(lo, hi)                    \
-  register_hybrid_pi1_##lo(t.hybrid[1]);   \
-  register_hybrid_pi2_##lo(t.hybrid[2]);
+#define PK_REGH(lo, hi)                         \
+  register_hybrid_pi1_w0_##lo(t.hybrid[0][1]);  \
+  register_hybrid_pi2_w0_##lo(t.hybrid[0][2]);  \
+  register_hybrid_pi1_w1_##lo(t.hybrid[1][1]);  \
+  register_hybrid_pi2_w1_##lo(t.hybrid[1][2]);
     PK_FOR_EACH_HYBRID_RANGE(PK_REGH)
 #undef PK_REGH
 #define PK_REGW1(lo, hi) register_wide_p1_##lo(t.wide[1]);
@@ -669,6 +671,7 @@ struct ModpGroup {
   int pf = 0;                  // trailing fp64 primes (hybrid kernel, lazy only)
   std::vector<int> idx;        // indices into the caller's prime list
   bool wide = false;           // Montgomery-64 walk: 64-bit residues, 2 output words per prime
+  bool wf = false;             // hybrid with a wide fp64 prime (fp64w_prime_ok, two-product)
   int out_words() const { return wide ? 2 * P : P; }
 };
 
@@ -695,22 +698,29 @@ static uint64_t fix_block(uint64_t raw, uint64_t p, int n) {
   if (!(p & 1)) return raw % p;
   return mulmod_h(raw % p, pow2mod_h(64ull * (n - 1), p), p);
 }
-// the group's residue matrices as the kernel reads them: uint32 for the 32-bit
-// kernels, uint64 for the wide walk
+// the group's residue matrices as the kernel reads them: uint32 for the
+// Montgomery-32 primes, uint64 for the wide walk and for the fp64 primes of a
+// hybrid group (after the uint32 part, padded to 8 bytes: hybrid_fp_offset)
 static std::vector<uint8_t> pack_residues(const ModpGroup& G, const uint64_t* a, size_t nn) {
-  const size_t wb = G.wide ? 8 : 4;
-  std::vector<uint8_t> h(G.idx.size() * nn * wb);
-  size_t o = 0;
-  for (int k : G.idx)
-    for (size_t e = 0; e < nn; ++e, o += wb) {
-      if (G.wide) {
-        const uint64_t v = a[k * nn + e];
-        std::memcpy(&h[o], &v, 8);
+  std::vector<uint8_t> h;
+  const int pi = G.P - G.pf;
+  for (int q = 0; q < G.P; ++q) {
+    const bool w64 = G.wide || q >= pi;
+    if (w64 && (h.size() & 7)) h.resize((h.size() + 7) & ~size_t(7), 0);
+    const uint64_t* aq = a + G.idx[q] * nn;
+    for (size_t e = 0; e < nn; ++e) {
+      const size_t o = h.size();
+      if (w64) {
+        h.resize(o + 8);
+        std::memcpy(&h[o], &aq[e], 8);
       } else {
-        const uint32_t v = static_cast<uint32_t>(a[k * nn + e]);
+        const uint32_t v = static_cast<uint32_t>(aq[e]);
+        h.resize(o + 4);
         std::memcpy(&h[o], &v, 4);
       }
     }
+  }
+  if (h.size() & 7) h.resize((h.size() + 7) & ~size_t(7), 0);  // next group stays aligned
   return h;
 }
 // one launch group's raw output words -> residues, stored at the caller's indices
@@ -781,7 +791,7 @@ static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, const ModpGroup& G, int
     PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing wide F_p kernel instantiation");
     L.smem = (2 * p.m + 1) * P * col_stride(p.n, 8) * 8;
   } else if (pf) {
-    L.fn = tables().hybrid[pi][p.n];
+    L.fn = tables().hybrid[G.wf ? 1 : 0][pi][p.n];
     PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing hybrid F_p kernel instantiation");
     const int int_words = ((2 * p.m + 1) * pi * col_stride(p.n, 4) + 1) & ~1;
     L.smem = int_words * 4 + (p.m + 1) * pf * col_stride(p.n, 8) * 8;
@@ -839,9 +849,11 @@ static std::vector<ModpGroup> group_primes(const std::vector<int>& fast, const u
                                            int n) {
   std::vector<ModpGroup> gs;
   const int pmax = max_primes_per_lane(n);
-  std::vector<int> fp, lz, red, wd;
+  std::vector<int> fp, fpw, lz, red, wd;
   for (int k : fast) {
-    if (wide_prime(primes[k]))
+    if (wide_prime(primes[k]) && fp64w_prime_ok(primes[k], n) && hybrid_available(n))
+      fpw.push_back(k);  // pairs with a lazy prime below, else the Montgomery-64 walk
+    else if (wide_prime(primes[k]))
       wd.push_back(k);
     else if (!lazy_prime(primes[k], n))
       red.push_back(k);
@@ -851,12 +863,18 @@ static std::vector<ModpGroup> group_primes(const std::vector<int>& fast, const u
       lz.push_back(k);
   }
   if (hybrid_available(n)) {
+    while (!fpw.empty() && !lz.empty()) {  // wide fp64 primes first: more bits per walk
+      gs.push_back(ModpGroup{2, true, 1, {lz.front(), fpw.front()}, false, true});
+      lz.erase(lz.begin());
+      fpw.erase(fpw.begin());
+    }
     while (!fp.empty() && !lz.empty()) {
       gs.push_back(ModpGroup{2, true, 1, {lz.front(), fp.front()}});
       lz.erase(lz.begin());
       fp.erase(fp.begin());
     }
   }
+  wd.insert(wd.end(), fpw.begin(), fpw.end());  // unpaired wide fp64 primes
   lz.insert(lz.end(), fp.begin(), fp.end());  // leftover small primes run as Montgomery
   for (int mode = 1; mode >= 0; --mode) {
     const std::vector<int>& sel = mode ? lz : red;

@@ -23,9 +23,11 @@ constexpr int kMaxP = 4;   // primes per lane in the F_p kernel
 // hybrid (Montgomery + fp64 primes) kernels exist for N in [kHybridMinN, kMaxN]
 constexpr int kHybridMinN = 17;
 #define PK_FOR_EACH_HYBRID_RANGE(X) X(17, 28) X(29, 36) X(37, 42) X(43, 48)
-#define PK_DECL_HYBRID(lo, hi)                      \
-  void register_hybrid_pi1_##lo(const void** tbl); \
-  void register_hybrid_pi2_##lo(const void** tbl);
+#define PK_DECL_HYBRID(lo, hi)                         \
+  void register_hybrid_pi1_w0_##lo(const void** tbl); \
+  void register_hybrid_pi2_w0_##lo(const void** tbl); \
+  void register_hybrid_pi1_w1_##lo(const void** tbl); \
+  void register_hybrid_pi2_w1_##lo(const void** tbl);
 PK_FOR_EACH_HYBRID_RANGE(PK_DECL_HYBRID)
 #undef PK_DECL_HYBRID
 // wide (2^31 <= p < 2^62, Montgomery-64) kernels: one prime per lane (two per

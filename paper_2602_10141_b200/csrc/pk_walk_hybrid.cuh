@@ -17,8 +17,20 @@
 // primes cover the same CRT bits as 4 Montgomery primes at 3/4 of the
 // fmaheavy time (n = 36: 3 x 25.8 + 24.4 >= 95 bits).
 //
+// Wide fp64 primes (WF, fp64w_prime_ok: n^2 p <= 2^50, ~2^39.7 at n = 36) use
+// the FMA two-product instead of an exact h:
+//   h = fl(a y), l = fma(a, y, -h)  (a y = h + l exactly)
+//   modmul(a, y) = fma(-rint(h / p), p, h) + l            (6 FP64 instructions)
+// The fma is exact (its true value is a small integer) and so is the final add,
+// so products stay signed integers with |y| < p (bound: |y| <= p/2 + 1.5 |h| 2^-52
+// and |h| <= n^2 p^2).  Chains start from the unreduced row sum, and the
+// per-lane sum is reduced once per step pair (|acc| < 3p).  At ~6 + 1 FP64
+// instructions per row update a wide prime carries ~40 bits against ~24.
+//
 // Residues of fp64 primes are plain (no Montgomery scale); Ryser's (-1)^n is
-// applied on the host like for the Montgomery primes.
+// applied on the host like for the Montgomery primes.  Residue matrices: the
+// PI Montgomery primes as uint32, padded to 8 bytes, then the PF fp64 primes
+// as uint64.
 #pragma once
 
 #include "pk_walk.cuh"
@@ -36,7 +48,13 @@ __host__ __device__ constexpr bool fp64_prime_ok(uint64_t p, int n) {
                  (static_cast<double>((p - 1) / 2) + 1.0) < 4503599627370496.0;
 }
 
-template <int N, int PF>
+__host__ __device__ constexpr bool fp64w_prime_ok(uint64_t p, int n) {
+  return (p & 1) && p >= 3 && p < (1ull << 50) &&
+         static_cast<double>(n) * static_cast<double>(n) * static_cast<double>(p) <=
+             1125899906842624.0;  // 2^50
+}
+
+template <int N, int PF, bool WF>
 struct FpPart {
   static constexpr int NS = col_stride(N, 8);
   static constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
@@ -50,8 +68,13 @@ struct FpPart {
     return fma(-qq, mc->fp[q], v);
   }
   __device__ __forceinline__ double modmul(double a, double y, int q) const {
-    const double h = a * y;  // exact: |h| < 2^53
-    return reduce(h, q);
+    const double h = a * y;  // exact when !WF: |h| < 2^53
+    if constexpr (WF) {
+      const double l = fma(a, y, -h);  // a y - h, exact
+      return reduce(h, q) + l;
+    } else {
+      return reduce(h, q);
+    }
   }
 
   // flip one column: x += sg * col (exact integers)
@@ -83,7 +106,10 @@ struct FpPart {
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         const int c = i % kC;
-        ch[c] = (i < kC) ? reduce(x[q][i], q) : modmul(x[q][i], ch[c], q);
+        if (i < kC)
+          ch[c] = WF ? x[q][i] : reduce(x[q][i], q);  // WF: chains start unreduced
+        else
+          ch[c] = modmul(x[q][i], ch[c], q);
       }
 #pragma unroll
       for (int w = 1; w < kC; w *= 2)
@@ -94,9 +120,13 @@ struct FpPart {
   }
 };
 
+// Offset (in uint32 words) of the fp64 primes' uint64 residues in the group's
+// residue array: the PI Montgomery matrices, padded to 8 bytes.
+__host__ __device__ constexpr int hybrid_fp_offset(int pi, int n) { return (pi * n * n + 1) & ~1; }
+
 template <int N, int PI, int PF>
-__device__ void stage_hybrid(uint32_t* sm, const uint32_t* a, const uint32_t* primes, int m,
-                             int algo, int tid, int nthreads) {
+__device__ void stage_hybrid(uint32_t* sm, const uint32_t* a, const uint32_t* primes,
+                             const uint64_t* fprimes, int m, int algo, int tid, int nthreads) {
   // Montgomery part (lazy rows) in the layout of stage_modp; primes [0, PI)
   stage_modp<N, PI, true>(sm, a, primes, m, algo, tid, nthreads);
   // fp64 part: Wf[m][PF][NS] then basef[PF][NS] (doubles), primes [PI, PI+PF)
@@ -110,9 +140,10 @@ __device__ void stage_hybrid(uint32_t* sm, const uint32_t* a, const uint32_t* pr
     const int i = idx % NS8;
     const int q = (idx / NS8) % PF;
     const int b = idx / (PF * NS8) - 1;  // -1: base
-    const uint32_t p = primes[PI + q];
-    const uint32_t* aq = a + (PI + q) * nn;
-    uint32_t v = 0;
+    const uint64_t p = fprimes[q];
+    const uint64_t* aq =
+        reinterpret_cast<const uint64_t*>(a + hybrid_fp_offset(PI, N)) + q * nn;
+    uint64_t v = 0;
     if (i < N) {
       if (b < 0) {
         if (algo == 1)
@@ -123,25 +154,25 @@ __device__ void stage_hybrid(uint32_t* sm, const uint32_t* a, const uint32_t* pr
       } else if (algo == 0) {
         v = aq[i * N + b];
       } else {
-        uint32_t two = aq[(b + 1) * N + i] * 2u;
+        uint64_t two = aq[(b + 1) * N + i] * 2u;
         two = two >= p ? two - p : two;
         v = two == 0 ? 0u : p - two;
       }
     }
-    (b < 0 ? basef : Wf + b * PF * NS8)[q * NS8 + i] = static_cast<double>(v);
+    (b < 0 ? basef : Wf + b * PF * NS8)[q * NS8 + i] = static_cast<double>(v);  // exact, < 2^50
   }
 }
 
-template <int N, int PI, int PF>
+template <int N, int PI, int PF, bool WF>
 struct HybridWalker {
   ModpWalker<N, PI, true> mw;
-  FpPart<N, PF> fw;
+  FpPart<N, PF, WF> fw;
 
   __device__ __forceinline__ void walk(const uint32_t* __restrict__ W2, const uint32_t* __restrict__ base,
                                        const double* __restrict__ Wf, const double* __restrict__ basef,
                                        int m, int k, uint64_t seg) {
     constexpr int CS = ModpWalker<N, PI, true>::CS;
-    constexpr int NS8 = FpPart<N, PF>::NS;
+    constexpr int NS8 = FpPart<N, PF, WF>::NS;
     const uint32_t* Wm = W2 + m * CS;
     const uint64_t start = seg << k;
     const uint64_t g = start ^ (start >> 1);
@@ -174,7 +205,10 @@ struct HybridWalker {
     auto pair = [&]() {
       mw.add_pair(ye, yo);
 #pragma unroll
-      for (int q = 0; q < PF; ++q) fw.acc[q] += fe[q] - fo[q];
+      for (int q = 0; q < PF; ++q) {
+        fw.acc[q] += fe[q] - fo[q];
+        if constexpr (WF) fw.acc[q] = fw.reduce(fw.acc[q], q);  // |acc| < 3p stays exact
+      }
     };
     // steps 0 (no flip) and 1
     mw.tree(ye);
@@ -204,13 +238,13 @@ struct HybridWalker {
 
 // One (Montgomery + fp64) prime group per launch (args.B == 1, constants in args.mc;
 // the residue matrices of the PI Montgomery primes come first, then the fp64 ones).
-template <int N, int PI, int PF>
+template <int N, int PI, int PF, bool WF>
 __global__ void __launch_bounds__(kWalkThreads, PK_HYB_MINCTA)
     walk_hybrid_kernel(const __grid_constant__ WalkArgs args) {
   constexpr int P = PI + PF;
   constexpr int NS4 = col_stride(N, 4);
   constexpr int NS8 = col_stride(N, 8);
-  using HW = HybridWalker<N, PI, PF>;
+  using HW = HybridWalker<N, PI, PF, WF>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem_raw);
   const int int_words = ((2 * args.m + 1) * PI * NS4 + 1) & ~1;
@@ -218,14 +252,11 @@ __global__ void __launch_bounds__(kWalkThreads, PK_HYB_MINCTA)
   const int lane = lane_id();
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWalkWarps + warp;
   const uint64_t tw = static_cast<uint64_t>(gridDim.x) * kWalkWarps;
-  // stage_hybrid reads the group's primes as uint32 [PI Montgomery..., PF fp64...]
-  uint32_t pr[P];
+  uint64_t fpr[PF];
 #pragma unroll
-  for (int q = 0; q < PI; ++q) pr[q] = args.mc.p[q];
-#pragma unroll
-  for (int q = 0; q < PF; ++q) pr[PI + q] = static_cast<uint32_t>(args.mc.fp[q]);
-  stage_hybrid<N, PI, PF>(slot, static_cast<const uint32_t*>(args.a), pr, args.m, args.algo,
-                          threadIdx.x, blockDim.x);
+  for (int q = 0; q < PF; ++q) fpr[q] = static_cast<uint64_t>(args.mc.fp[q]);
+  stage_hybrid<N, PI, PF>(slot, static_cast<const uint32_t*>(args.a), args.mc.p, fpr, args.m,
+                          args.algo, threadIdx.x, blockDim.x);
   __syncthreads();
   HW w;
   w.mw.mc = &args.mc;

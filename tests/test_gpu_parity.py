@@ -287,6 +287,27 @@ def test_engine_kats(gpu):
         assert abs(got - ref) <= 1e-11 * abs(ref)
 
 
+def test_ryser_glynn_naive_100_matrices_per_domain(gpu):
+    """SPEC engine property: Ryser = Glynn = naive for n <= 8 on >= 100 matrices per
+    domain (complex, real: batched GPU walks; integer and F_p: exact paths)."""
+    rng = np.random.default_rng(2602)
+    for n in range(1, 9):
+        zc = rng.standard_normal((100, n, n)) + 1j * rng.standard_normal((100, n, n))
+        zr = rng.standard_normal((100, n, n))
+        for z in (zc, zr):
+            naive = np.array([engine.perm_naive(m) for m in z])
+            # every term is bounded by prod_i sum_j |a_ij|; there are <= 2^n of them
+            scale = np.array([np.prod(np.abs(m).sum(axis=1)) for m in z]) * 2.0 ** n
+            for method in ("ryser", "glynn"):
+                got = perm_batch(z, method=method)
+                assert np.all(np.abs(got - naive) <= 4 * n * U * scale + 1e-300), (n, method)
+        for k in range(13):  # exact domains through the scalar API (104 matrices)
+            ints = rng.integers(-9, 10, size=(n, n)).tolist()
+            naive = engine.perm_naive(ints)
+            assert engine.perm_ryser(ints) == naive == engine.perm_glynn(ints)
+            assert engine.perm_glynn(ints, PrimeField(1000003)) == naive % 1000003
+
+
 def test_blocked_determinism_and_properties(gpu):
     a = ensembles.sample_matrix("ginibre-c", 14, 9, 0)
     plan = make_block_plan(14, "ryser", 64)
@@ -353,11 +374,13 @@ def test_schur_resumable_checkpoint(gpu, tmp_path):
         modular.schur_permanent_resumable(25, str(ck), chunks=16)
 
 
-def test_hybrid_fp64_primes_vs_oracle(gpu):
-    """Montgomery + fp64 primes walked together (hybrid kernel) are exact."""
+@pytest.mark.parametrize("fkind", ["fp64", "fp64w"])
+def test_hybrid_fp64_primes_vs_oracle(gpu, fkind):
+    """Montgomery + fp64 primes walked together (hybrid kernel) are exact, for the
+    narrow (exact-product) and wide (two-product, ~40-bit) fp64 primes."""
     rng = np.random.default_rng(17)
     for n in (20, 29, 36, 43):
-        primes = modular.prime_pool(n, "lazy", 2) + modular.prime_pool(n, "fp64", 2)
+        primes = modular.prime_pool(n, "lazy", 2) + modular.prime_pool(n, fkind, 2)
         mats = np.stack([modular._root_matrix_u64(n, p, modular.primitive_nth_root(p, n))
                          for p in primes])
         for algo in ("ryser", "glynn"):

@@ -178,28 +178,35 @@ def test_crt_round_trip_and_basis_checks():
         modular.schur_permanent_exact(49)
 
 
+def _basis_kinds(b, n):
+    return [("fp64w" if p >= 2 ** 31 and modular.fp64w_prime_ok(p, n) else
+             "fp64" if modular.fp64_prime_ok(p, n) else
+             "lazy" if n * (p - 1) < 2 ** 31 else "red") for p in b.primes]
+
+
 def test_gpu_prime_basis_properties():
     for n in (2, 13, 17, 30, 35, 36, 37, 41, 43, 48):
         b = modular.gpu_prime_basis(n)
         for p in b.primes:
-            assert (p - 1) % n == 0 and modular.is_probable_prime(p) and p < 2 ** 31
+            assert (p - 1) % n == 0 and modular.is_probable_prime(p)
+            assert p < 2 ** 31 or modular.fp64w_prime_ok(p, n)
         assert b.product > 4 * modular._perm_bound(n) + 1
-        kinds = [("fp64" if modular.fp64_prime_ok(p, n) else
-                  "lazy" if n * (p - 1) < 2 ** 31 else "red") for p in b.primes]
-        cost = modular.basis_walk_seconds(n, kinds.count("red"), kinds.count("lazy"),
-                                          kinds.count("fp64"))
-        # no worse than the reference-style all-31-bit basis or an all-lazy basis
+        k = _basis_kinds(b, n)
+        cost = modular.basis_walk_seconds(n, k.count("red"), k.count("lazy"), k.count("fp64"),
+                                          k.count("fp64w"))
+        # no worse than the reference-style all-31-bit basis
         ref31 = len(modular.find_primes(n, max_bits=31).primes)
         assert cost <= modular.basis_walk_seconds(n, ref31, 0, 0) + 1e-12
-    assert len(modular.gpu_prime_basis(36).primes) == 4
-    # n = 36: two (lazy, fp64) hybrid pairs; n = 43: four reduced primes (3 + 1)
-    assert [modular.fp64_prime_ok(p, 36) for p in modular.gpu_prime_basis(36).primes].count(True) == 2
-    assert all(43 * (p - 1) >= 2 ** 31 for p in modular.gpu_prime_basis(43).primes)
+        assert k.count("fp64w") <= k.count("lazy")  # every wide fp64 prime has a partner
+    assert 3 <= len(modular.gpu_prime_basis(36).primes) <= 4
     assert modular._launch_groups(43, 4, 0, 0) == [("red", 3), ("red", 1)]
     assert modular._launch_groups(36, 0, 2, 2) == [("hyb", 2), ("hyb", 2)]
-    for kind in ("reduced", "lazy", "fp64"):
+    assert modular._launch_groups(36, 1, 1, 0, 1) == [("hybw", 2), ("red", 1)]
+    assert modular._launch_groups(36, 0, 0, 0, 1) == [("wide", 1)]
+    for kind in ("reduced", "lazy", "fp64", "fp64w"):
         pool = modular.prime_pool(36, kind, 3)
         assert len(pool) == 3 and pool == sorted(pool, reverse=True)
+    assert all(p >= 2 ** 31 and 36 * 36 * p <= 2 ** 50 for p in modular.prime_pool(36, "fp64w", 3))
 
 
 def test_integer_crt_primes_cover_bound():

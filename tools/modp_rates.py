@@ -6,7 +6,8 @@ For each n it times one resident walk over an aligned Gray range of 2^bits indic
 (per-step cost is start-independent) for every launch-group shape the C ABI forms:
   red<P>   P reduced 31-bit Montgomery primes   (n (p - 1) >= 2^31)
   lazy<P>  P lazy Montgomery primes             (n (p - 1) < 2^31, not fp64-eligible)
-  hyb11    one lazy Montgomery prime + one fp64 prime (walk_hybrid_kernel<n, 1, 1>)
+  hyb11    one lazy Montgomery prime + one fp64 prime (walk_hybrid_kernel<n, 1, 1, false>)
+  hybw11   one lazy Montgomery prime + one wide fp64 prime (walk_hybrid_kernel<n, 1, 1, true>)
   wide<P>  P 59-bit primes, Montgomery-64 (walk_modp64_kernel<n, P>)
 and reports prime-row-updates/s and CRT bits/s (sum of log2 p per second).
 """
@@ -69,6 +70,7 @@ def main():
         shapes.update({f"lazy{P}": lazy[:P] for P in range(1, pmax + 1)})
         if n >= 17:
             shapes["hyb11"] = [lazy[0], fp[0]]
+            shapes["hybw11"] = [lazy[0], modular.prime_pool(n, "fp64w", 1)[0]]
         wide = primes_desc(n, 1 << 59, 2, lambda p: True)  # reference default 59-bit basis
         shapes["wide1"] = wide[:1]
         if n <= 36:
