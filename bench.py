@@ -335,8 +335,8 @@ def secondary(args, nat, modular):
     t0 = time.perf_counter()
     value, b, wit = modular.schur_permanent_fast(args.schur_n)
     sec["schur_exact"] = {"n": args.schur_n, "value": str(value), "primes": list(b.primes),
-                          "wall_s": time.perf_counter() - t0,
-                          "row_updates": len(b.primes) * args.schur_n * 2.0 ** args.schur_n}
+                          "wall_s": time.perf_counter() - t0, "expansion": "glynn",
+                          "row_updates": len(b.primes) * args.schur_n * 2.0 ** (args.schur_n - 1)}
     return sec
 
 

@@ -196,6 +196,10 @@ def _crt_lift(residues, primes) -> int:
 
 
 def _exact_int_perm(rows, n: int, algorithm: str, devices) -> int:
+    # The exact value does not depend on the expansion, so the walk is always
+    # Glynn's: 2^(n-1) sign vectors instead of Ryser's 2^n subsets, same cost
+    # per step (the CRT primes are odd, so 2^(n-1) is invertible).
+    algorithm = GLYNN
     bound = 1
     for r in rows:
         bound *= sum(abs(int(v)) for v in r)

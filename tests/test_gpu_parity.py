@@ -213,6 +213,12 @@ def test_schur_exact_values_match_reference(gpu):
         assert [w.prime for w in wit] == row["primes"]
         assert [w.residue for w in wit] == row["residues"]
         assert [w.root for w in wit] == row["roots"]
+    # the residue does not depend on the expansion: Glynn (default) == Ryser (reference)
+    for n in (1, 2, 5, 13, 21, 23):
+        for bits in (31, 59):
+            _, _, wg = modular.schur_permanent_exact(n, max_bits=bits)
+            _, _, wr = modular.schur_permanent_exact(n, max_bits=bits, method="ryser")
+            assert [w.residue for w in wg] == [w.residue for w in wr], (n, bits)
     h = g["helpers"]
     assert modular.schur_residue(3, 7, root=2).residue == h["residue_3_7_g2"]
     assert modular.schur_residue(2, 5, root=4).residue == h["residue_2_5_g4"]
@@ -372,6 +378,11 @@ def test_schur_resumable_checkpoint(gpu, tmp_path):
     assert done == 8 and v == -5198937484375
     with pytest.raises(ValueError, match="different run"):
         modular.schur_permanent_resumable(25, str(ck), chunks=16)
+    with pytest.raises(ValueError, match="different run"):
+        modular.schur_permanent_resumable(25, str(ck), chunks=8, method="ryser")
+    v, _, _, done = modular.schur_permanent_resumable(25, str(tmp_path / "r25.jsonl"), chunks=4,
+                                                      method="ryser")
+    assert done == 4 and v == -5198937484375
 
 
 @pytest.mark.parametrize("fkind", ["fp64", "fp64w"])

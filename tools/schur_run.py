@@ -1,6 +1,7 @@
-"""C4 runs: exact perm(S_n) for large odd n on one B200, cross-checked on a second prime basis.
+"""C4 runs: exact perm(S_n) for large odd n on one B200, cross-checked on a second prime
+basis (31-bit, Ryser expansion: an independent walk).
 
-    python tools/schur_run.py 37 39 41 43 [--check 37 39]  -> gpurun_out/schur_c4.json
+    python tools/schur_run.py 37 39 41 43 [--check 37 39] [--method glynn|ryser]
 """
 import argparse
 import json
@@ -17,19 +18,21 @@ def main():
     ap.add_argument("ns", type=int, nargs="+")
     ap.add_argument("--check", type=int, nargs="*", default=[])
     ap.add_argument("--out", default="gpurun_out/schur_c4.json")
+    ap.add_argument("--method", default="glynn", choices=["glynn", "ryser"])
     args = ap.parse_args()
     rows = []
     modular.schur_permanent_fast(21)  # warm-up (context, module load)
     for n in args.ns:
         t0 = time.perf_counter()
-        v, b, w = modular.schur_permanent_fast(n)
+        v, b, w = modular.schur_permanent_fast(n, method=args.method)
         dt = time.perf_counter() - t0
+        upd = len(b.primes) * n * 2.0 ** (n - 1 if args.method == "glynn" else n)
         row = {"n": n, "value": str(v), "basis": list(b.primes), "residues": [x.residue for x in w],
-               "wall_s": dt, "row_updates": len(b.primes) * n * 2.0 ** n,
-               "prime_updates_per_s": len(b.primes) * n * 2.0 ** n / dt}
+               "expansion": args.method, "wall_s": dt, "row_updates": upd,
+               "prime_updates_per_s": upd / dt}
         if n in args.check:
             t0 = time.perf_counter()
-            v2, b2, w2 = modular.schur_permanent_exact(n, max_bits=31)
+            v2, b2, w2 = modular.schur_permanent_exact(n, max_bits=31, method="ryser")
             row["check_basis"] = list(b2.primes)
             row["check_value"] = str(v2)
             row["check_wall_s"] = time.perf_counter() - t0
