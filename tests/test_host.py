@@ -4,6 +4,7 @@ samplers, geodesic matrices, input validation and the C-ABI library surface.
 Golden values come from the reference (tests/golden/, tools/make_golden.py).
 """
 import ctypes
+import os
 import re
 from fractions import Fraction
 
@@ -242,6 +243,22 @@ def test_sample_batch_thread_invariant():
         ensembles.EnsembleSpec("gue", 0, 1, 0)
     with pytest.raises(ValueError, match="spec is not GUE"):
         ensembles.sample_gue(ensembles.EnsembleSpec("goe", 3, 1, 0))
+
+
+def test_sampler_pool_only_for_spawn_safe_mains(tmp_path):
+    """A spawn child re-runs an unguarded __main__ script, so the pool is skipped there."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    body = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2602_10141_b200 import ensembles as e\n" % root)
+    unguarded = tmp_path / "u.py"
+    unguarded.write_text(body + "print(e._spawn_safe())\n")
+    guarded = tmp_path / "g.py"
+    guarded.write_text(body + 'if __name__ == "__main__":\n    print(e._spawn_safe())\n')
+    out = [subprocess.run([sys.executable, str(f)], capture_output=True, text=True,
+                          timeout=120).stdout.strip() for f in (unguarded, guarded)]
+    assert out == ["False", "True"]
 
 
 def test_sample_batch_process_pool_bit_identical():
