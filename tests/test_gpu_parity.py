@@ -113,6 +113,23 @@ def test_full_permanent_vs_oracle(gpu, kind, n, algo):
         assert isinstance(api, float)
 
 
+@pytest.mark.parametrize("kind,n,algo", [("haar-u", 40, "ryser"), ("haar-u", 44, "glynn"),
+                                         ("haar-o", 48, "ryser"), ("ginibre-c", 48, "glynn")])
+def test_large_n_tile_vs_oracle(gpu, kind, n, algo):
+    """Maximum sizes: one whole tile (32 segments of 2^k, k = m - 22) of the n = 40-48
+    kernels, including the complex instantiations that spill, against the oracle."""
+    a = ensembles.sample_matrix(kind, n, 2602, 5)
+    m = n if algo == "ryser" else n - 1
+    span = 1 << (m - 17)  # one tile
+    st = int(np.random.default_rng(n).integers(0, 1 << 17)) * span
+    parts = 64
+    rows = oracle.run_blocks(a, [st + i * (span // parts) for i in range(parts)],
+                             [span // parts] * parts, algo)
+    ref = oracle.kahan_combine(rows, np.iscomplexobj(a))
+    s, c, ab = gpu.ryser_f64(a, algo, st, span, want_abs=True)
+    assert abs(complex(s + c) - ref) <= 8 * n * U * ab + 4 * U * abs(ref), (kind, n, algo)
+
+
 def test_unaligned_ranges_and_ragged_pieces(gpu):
     a = ensembles.sample_matrix("ginibre-c", 16, 3, 0)
     rng = np.random.default_rng(7)
@@ -203,6 +220,30 @@ def test_modp_random_blocks_vs_oracle_large_n(gpu):
                     a, [st + k * (ln // 32) for k in range(32)], [ln // 32] * 32, algo, p=p)) % p)
                 fn = kernels.ryser_partial_modp if algo == "ryser" else kernels.glynn_partial_modp
                 assert fn(a, st, ln, p) == want, (n, p, algo, "long")
+
+
+@pytest.mark.parametrize("n", [44, 48])
+def test_modp_large_n_tile_vs_oracle(gpu, n):
+    """One whole tile of the n = 44 / 48 F_p kernels for every launch-group kind the basis
+    model and the C ABI form (reduced, lazy, hybrid narrow / wide, Montgomery-64)."""
+    primes = (modular.prime_pool(n, "reduced", 1) + modular.prime_pool(n, "lazy", 2)
+              + modular.prime_pool(n, "fp64", 1) + modular.prime_pool(n, "fp64w", 1)
+              + list(modular.find_primes(n, max_bits=59).primes[:1]))
+    mats = np.stack([modular._root_matrix_u64(n, p, modular.primitive_nth_root(p, n))
+                     for p in primes])
+    algo = "glynn" if n == 44 else "ryser"
+    m = n if algo == "ryser" else n - 1
+    span = 1 << (m - 17)
+    if n == 48:  # 2^31-index tile: keep the CPU oracle to seconds (one reduced, one lazy)
+        primes, mats = primes[:2], mats[:2]
+    st = 5 * span
+    got = gpu.ryser_modp(mats, primes, algo, st, span)
+    parts = 64
+    for q, p in enumerate(primes):
+        want = int(sum(int(x) for x in oracle.run_blocks(
+            mats[q], [st + i * (span // parts) for i in range(parts)], [span // parts] * parts,
+            algo, p=p)) % p)
+        assert got[q] == want, (n, p, algo)
 
 
 def test_schur_exact_values_match_reference(gpu):
