@@ -297,25 +297,36 @@ struct F64Walker {
     }
   }
 
-  // Walk segment `seg` (2^k indices starting at seg << k).
+  static constexpr int kSubBits = 12;
   __device__ __forceinline__ void walk(const T* __restrict__ base, const T* __restrict__ W, int m,
                                        int k, uint64_t seg) {
+    s_re = c_re = s_im = c_im = abs_acc = 0.0;
+    const int ks = min(k, kSubBits);
+    const uint32_t nsub = 1u << (k - ks);
+    for (uint32_t i = 0; i < nsub; ++i) walk_sub(base, W, m, ks, (seg << (k - ks)) | i);
+  }
+
+  // Walk segment `seg` (2^k indices starting at seg << k).
+  __device__ __forceinline__ void walk_sub(const T* __restrict__ base, const T* __restrict__ W,
+                                           int m, int k, uint64_t seg) {
     const uint64_t start = seg << k;
     const uint64_t g = start ^ (start >> 1);
+    const T* bp = base + (start >> 63) * NS;  // not hoisted out of the sub-segment loop
 #pragma unroll
-    for (int j = 0; j < N; ++j) r[j] = base[j];
+    for (int j = 0; j < N; ++j) r[j] = bp[j];
     for (int b = k - 1; b < m; ++b) {  // start state: columns set in gray(start)
       const double on = ((g >> b) & 1) ? 1.0 : 0.0;
       const T* col = W + b * NS;
 #pragma unroll
       for (int j = 0; j < N; ++j) fma_upd(r[j], on, col[j]);
     }
-    s_re = c_re = s_im = c_im = abs_acc = 0.0;
     const uint32_t L = 1u << k;
     const bool lane_minus = seg & 1;
     {  // steps 0 (no flip) and 1
       const T pe = tree();
-      const T po = step(W, StepPlan::minus_odd(1, k, lane_minus) ? -1.0 : 1.0);
+      // (start >> 63) is always 0: keeps column 0 from being hoisted out of the
+      // sub-segment loop into registers
+      const T po = step(W + (start >> 63) * NS, StepPlan::minus_odd(1, k, lane_minus) ? -1.0 : 1.0);
       add_pair(pe, po);
     }
     for (uint32_t e = 2; e < L; e += 2) {
