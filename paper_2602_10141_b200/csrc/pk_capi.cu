@@ -794,7 +794,7 @@ static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, const ModpGroup& G, int
     L.fn = tables().hybrid[G.wf ? 1 : 0][pi][p.n];
     PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing hybrid F_p kernel instantiation");
     const int int_words = ((2 * p.m + 1) * pi * col_stride(p.n, 4) + 1) & ~1;
-    L.smem = int_words * 4 + (p.m + 1) * pf * col_stride(p.n, 8) * 8;
+    L.smem = int_words * 4 + (2 * p.m + 1) * pf * col_stride(p.n, 8) * 8;
   } else {
     L.fn = tables().modp[lazy ? 1 : 0][P][p.n];
     PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing F_p kernel instantiation");

@@ -77,19 +77,20 @@ struct FpPart {
     }
   }
 
-  // flip one column: x += sg * col (exact integers)
-  __device__ __forceinline__ void flip(const double* __restrict__ col, double sg) {
+  // flip one column: x += col, col the plus or minus copy (exact integers); a
+  // two-operand DADD reads fewer registers than fma(sg, col, x)
+  __device__ __forceinline__ void flip(const double* __restrict__ col) {
 #pragma unroll
     for (int q = 0; q < PF; ++q)
 #pragma unroll
       for (int j = 0; j + 2 <= N; j += 2) {
         const double2 c = *reinterpret_cast<const double2*>(col + q * NS + j);
-        x[q][j] = fma(sg, c.x, x[q][j]);
-        x[q][j + 1] = fma(sg, c.y, x[q][j + 1]);
+        x[q][j] += c.x;
+        x[q][j + 1] += c.y;
       }
     if constexpr (N & 1) {
 #pragma unroll
-      for (int q = 0; q < PF; ++q) x[q][N - 1] = fma(sg, col[q * NS + N - 1], x[q][N - 1]);
+      for (int q = 0; q < PF; ++q) x[q][N - 1] += col[q * NS + N - 1];
     }
   }
 
@@ -129,12 +130,13 @@ __device__ void stage_hybrid(uint32_t* sm, const uint32_t* a, const uint32_t* pr
                              const uint64_t* fprimes, int m, int algo, int tid, int nthreads) {
   // Montgomery part (lazy rows) in the layout of stage_modp; primes [0, PI)
   stage_modp<N, PI, true>(sm, a, primes, m, algo, tid, nthreads);
-  // fp64 part: Wf[m][PF][NS] then basef[PF][NS] (doubles), primes [PI, PI+PF)
+  // fp64 part: Wf[2 dir][m][PF][NS] (plus, minus copies) then basef[PF][NS] (doubles),
+  // primes [PI, PI+PF)
   constexpr int NS4 = col_stride(N, 4);
   constexpr int NS8 = col_stride(N, 8);
   const int int_words = ((2 * m + 1) * PI * NS4 + 1) & ~1;
   double* Wf = reinterpret_cast<double*>(sm + int_words);
-  double* basef = Wf + m * PF * NS8;
+  double* basef = Wf + 2 * m * PF * NS8;
   const int nn = N * N;
   for (int idx = tid; idx < (m + 1) * PF * NS8; idx += nthreads) {
     const int i = idx % NS8;
@@ -159,7 +161,13 @@ __device__ void stage_hybrid(uint32_t* sm, const uint32_t* a, const uint32_t* pr
         v = two == 0 ? 0u : p - two;
       }
     }
-    (b < 0 ? basef : Wf + b * PF * NS8)[q * NS8 + i] = static_cast<double>(v);  // exact, < 2^50
+    const double dv = static_cast<double>(v);  // exact, < 2^50
+    if (b < 0) {
+      basef[q * NS8 + i] = dv;
+    } else {
+      Wf[b * PF * NS8 + q * NS8 + i] = dv;
+      Wf[(m + b) * PF * NS8 + q * NS8 + i] = -dv;
+    }
   }
 }
 
@@ -174,6 +182,7 @@ struct HybridWalker {
     constexpr int CS = ModpWalker<N, PI, true>::CS;
     constexpr int NS8 = FpPart<N, PF, WF>::NS;
     const uint32_t* Wm = W2 + m * CS;
+    const double* Wfm = Wf + m * PF * NS8;  // minus copies
     const uint64_t start = seg << k;
     const uint64_t g = start ^ (start >> 1);
 #pragma unroll
@@ -191,7 +200,7 @@ struct HybridWalker {
         for (int q = 0; q < PI; ++q)
 #pragma unroll
           for (int j = 0; j < N; ++j) mw.r[q][j] += col[q * ModpWalker<N, PI, true>::NS + j];
-        fw.flip(Wf + b * PF * NS8, 1.0);
+        fw.flip(Wf + b * PF * NS8);
       }
     }
 #pragma unroll
@@ -216,7 +225,7 @@ struct HybridWalker {
     {
       const bool mi = StepPlan::minus_odd(1, k, lane_minus);
       mw.step(mi ? Wm : W2, yo);
-      fw.flip(Wf, mi ? -1.0 : 1.0);
+      fw.flip(mi ? Wfm : Wf);
       fw.product(fo);
       pair();
     }
@@ -224,12 +233,12 @@ struct HybridWalker {
       const int b = __ffs(e) - 1;
       const bool me = StepPlan::minus_even(e, k, lane_minus);
       mw.step((me ? Wm : W2) + b * CS, ye);
-      fw.flip(Wf + b * PF * NS8, me ? -1.0 : 1.0);
+      fw.flip((me ? Wfm : Wf) + b * PF * NS8);
       fw.product(fe);
       const bool mo = StepPlan::minus_odd(e + 1, k, lane_minus);
       // (e >> 31) is always 0: keeps column 0 from being hoisted into registers
       mw.step((mo ? Wm : W2) + (e >> 31) * CS, yo);
-      fw.flip(Wf + (e >> 31) * PF * NS8, mo ? -1.0 : 1.0);
+      fw.flip((mo ? Wfm : Wf) + (e >> 31) * PF * NS8);
       fw.product(fo);
       pair();
     }
@@ -267,7 +276,7 @@ __global__ void __launch_bounds__(kWalkThreads, PK_HYB_MINCTA)
   const uint32_t* W2 = slot;
   const uint32_t* base = slot + 2 * args.m * ModpWalker<N, PI, true>::CS;
   const double* Wf = reinterpret_cast<const double*>(slot + int_words);
-  const double* basef = Wf + args.m * PF * NS8;
+  const double* basef = Wf + 2 * args.m * PF * NS8;
   for (uint64_t tl = gw; tl < args.tiles; tl += tw) {
     const uint64_t seg = ((args.tile0 + tl) << kTileBits) + lane;
     const bool active = seg < args.segs_total;
