@@ -155,7 +155,9 @@ __device__ __forceinline__ void neumaier(double& s, double& c, double v) {
 }
 
 // Stage one matrix in walk form: base[NS] then W[m][NS] (NS = padded n).
-template <int N, bool CPLX>
+// Shared layout: base[NS] | W[m][NS] (| Wm[m][NS] = -W when MINUS: the
+// single-matrix kernels flip even-step columns with a two-operand DADD).
+template <int N, bool CPLX, bool MINUS = false>
 __device__ void stage_f64(typename F64T<CPLX>::T* sm, const double* a, int m, int algo, int tid,
                           int nthreads) {
   using F = F64T<CPLX>;
@@ -194,6 +196,16 @@ __device__ void stage_f64(typename F64T<CPLX>::T* sm, const double* a, int m, in
       }
     }
     (b < 0 ? base : W + b * NS)[i] = v;
+    if (MINUS && b >= 0) {
+      T nv = v;
+      if constexpr (CPLX) {
+        nv.x = -v.x;
+        nv.y = -v.y;
+      } else {
+        nv = -v;
+      }
+      W[(m + b) * NS + i] = nv;
+    }
   }
 }
 
@@ -331,7 +343,11 @@ struct F64Walker {
     }
     for (uint32_t e = 2; e < L; e += 2) {
       const int b = __ffs(e) - 1;
-      const T pe = step(W + b * NS, StepPlan::minus_even(e, k, lane_minus) ? -1.0 : 1.0);
+      // C0P kernels keep minus copies (Wm = W + m NS): the update is a DADD,
+      // +1.5 % against fma(+-1, col, r) (profiles/r1_walk_experiments_c0.txt)
+      const bool me = StepPlan::minus_even(e, k, lane_minus);
+      const T pe = C0P ? step((me ? W + m * NS : W) + b * NS, 1.0)
+                       : step(W + b * NS, me ? -1.0 : 1.0);
       // shared-memory column 0: (e >> 31) is always 0; it keeps the column
       // from being hoisted out of the loop into registers (spilling the state)
       const T* c = C0P ? c0 : W + (e >> 31) * NS;
@@ -372,7 +388,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
   constexpr int NS = W_::NS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
-  const int slot_elems = (args.m + 1) * NS;
+  const int slot_elems = ((C0P ? 2 : 1) * args.m + 1) * NS;
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   T* slot = smem + (args.per_warp_slot ? warp * slot_elems : 0);
@@ -385,7 +401,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
 
   int staged = -1;
   if (!args.per_warp_slot) {
-    stage_f64<N, CPLX>(slot, amat, args.m, args.algo, threadIdx.x, blockDim.x);
+    stage_f64<N, CPLX, C0P>(slot, amat, args.m, args.algo, threadIdx.x, blockDim.x);
     __syncthreads();
     staged = 0;
   }
@@ -401,7 +417,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
     const uint64_t tl = u % args.tiles;
     if (b != staged) {  // warp-uniform; only in per-warp-slot mode
       __syncwarp();
-      stage_f64<N, CPLX>(slot, amat + b * mat_stride, args.m, args.algo, lane, 32);
+      stage_f64<N, CPLX, C0P>(slot, amat + b * mat_stride, args.m, args.algo, lane, 32);
       __syncwarp();
       staged = b;
     }

@@ -31,7 +31,8 @@ int main(int argc, char** argv) {
 #endif
   const void* fn = (const void*)&walk_f64_kernel<N, CPLX, C0P>;
   const int eb = CPLX ? 16 : 8;
-  const int smem = (m + 1) * col_stride(n, eb) * eb;
+  const int smem = ((C0P ? 2 : 1) * m + 1) * col_stride(n, eb) * eb;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int occ = 0, sms = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWalkThreads, smem);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
