@@ -275,7 +275,8 @@ static F64Launch prepare_f64(DevCtx& c, const Plan& p, bool cplx, int algo, int 
   PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing fp64 kernel instantiation");
   L.per_warp = B > 1 ? 1 : 0;
   const int elem = cplx ? 16 : 8;
-  const int slot = ((c0p ? 2 : 1) * p.m + 1) * col_stride(p.n, elem) * elem;  // C0P: minus copies
+  // minus copies of the columns: F64Walker::kMinus (the C0P kernels)
+  const int slot = ((c0p ? 2 : 1) * p.m + 1) * col_stride(p.n, elem) * elem;
   L.smem = slot * (L.per_warp ? kWalkWarps : 1);
   L.occ = occupancy(c, L.fn, kWalkThreads, L.smem);
   const uint64_t units = static_cast<uint64_t>(B) * nt;

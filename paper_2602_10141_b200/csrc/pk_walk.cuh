@@ -223,6 +223,9 @@ struct F64Walker {
   double s_re, c_re, s_im, c_im, abs_acc;
   bool want_abs;
   const T* c0;  // C0P: column 0 in the __grid_constant__ parameter
+  // shared minus copies of the walk columns (DADD flips): single-matrix kernels
+  // only; in the batched kernels (a slot per warp) they measured -1 to -15 %
+  static constexpr bool kMinus = C0P;
 
   // Product of the state as a binary tree evaluated depth-first (a binary
   // counter over the leaves): the same N - 1 multiplies as a chain, depth
@@ -338,20 +341,24 @@ struct F64Walker {
       const T pe = tree();
       // (start >> 63) is always 0: keeps column 0 from being hoisted out of the
       // sub-segment loop into registers
-      const T po = step(W + (start >> 63) * NS, StepPlan::minus_odd(1, k, lane_minus) ? -1.0 : 1.0);
+      const bool mo = StepPlan::minus_odd(1, k, lane_minus);
+      const T po = kMinus ? step((mo ? W + m * NS : W) + (start >> 63) * NS, 1.0)
+                          : step(W + (start >> 63) * NS, mo ? -1.0 : 1.0);
       add_pair(pe, po);
     }
     for (uint32_t e = 2; e < L; e += 2) {
       const int b = __ffs(e) - 1;
-      // C0P kernels keep minus copies (Wm = W + m NS): the update is a DADD,
-      // +1.5 % against fma(+-1, col, r) (profiles/r1_walk_experiments_c0.txt)
+      // with minus copies (Wm = W + m NS) the update is a DADD: +1.5 % against
+      // fma(+-1, col, r) (profiles/r1_walk_experiments_c0.txt)
       const bool me = StepPlan::minus_even(e, k, lane_minus);
-      const T pe = C0P ? step((me ? W + m * NS : W) + b * NS, 1.0)
-                       : step(W + b * NS, me ? -1.0 : 1.0);
+      const T pe = kMinus ? step((me ? W + m * NS : W) + b * NS, 1.0)
+                          : step(W + b * NS, me ? -1.0 : 1.0);
       // shared-memory column 0: (e >> 31) is always 0; it keeps the column
       // from being hoisted out of the loop into registers (spilling the state)
-      const T* c = C0P ? c0 : W + (e >> 31) * NS;
-      const T po = step(c, StepPlan::minus_odd(e + 1, k, lane_minus) ? -1.0 : 1.0);
+      const bool mo = StepPlan::minus_odd(e + 1, k, lane_minus);
+      const T po = C0P      ? step(c0, mo ? -1.0 : 1.0)
+                   : kMinus ? step((mo ? W + m * NS : W) + (e >> 31) * NS, 1.0)
+                            : step(W + (e >> 31) * NS, mo ? -1.0 : 1.0);
       add_pair(pe, po);
     }
   }
@@ -388,7 +395,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
   constexpr int NS = W_::NS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
-  const int slot_elems = ((C0P ? 2 : 1) * args.m + 1) * NS;
+  const int slot_elems = ((W_::kMinus ? 2 : 1) * args.m + 1) * NS;
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   T* slot = smem + (args.per_warp_slot ? warp * slot_elems : 0);
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
 
   int staged = -1;
   if (!args.per_warp_slot) {
-    stage_f64<N, CPLX, C0P>(slot, amat, args.m, args.algo, threadIdx.x, blockDim.x);
+    stage_f64<N, CPLX, W_::kMinus>(slot, amat, args.m, args.algo, threadIdx.x, blockDim.x);
     __syncthreads();
     staged = 0;
   }
@@ -417,7 +424,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
     const uint64_t tl = u % args.tiles;
     if (b != staged) {  // warp-uniform; only in per-warp-slot mode
       __syncwarp();
-      stage_f64<N, CPLX, C0P>(slot, amat + b * mat_stride, args.m, args.algo, lane, 32);
+      stage_f64<N, CPLX, W_::kMinus>(slot, amat + b * mat_stride, args.m, args.algo, lane, 32);
       __syncwarp();
       staged = b;
     }
