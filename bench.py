@@ -326,10 +326,12 @@ def secondary(args, nat, modular):
     job.close()
     # C2-style batched sampler (ensembles.sample_permanents): host sampling (a process
     # pool) overlapped with the batched GPU walk; an 8,192-sample slice (two chunks) of
-    # the 50,000-sample config.  The warm-up call starts the sampler's process pool.
+    # the 50,000-sample config.  The warm-up call (the same slice) starts the sampler's
+    # process pool and brings the GPU out of its idle clocks: a first call after ~1 s of
+    # GPU idle (the CPU-baseline leg) measured up to 2x slower (gpurun_out batch A/B logs).
     from paper_2602_10141_b200 import ensembles
     spec = ensembles.EnsembleSpec("haar-u", 23, 8192, SEED)
-    ensembles.sample_permanents(ensembles.EnsembleSpec("haar-u", 23, 1024, SEED))
+    ensembles.sample_permanents(spec)
     t0 = time.perf_counter()
     vals = ensembles.sample_permanents(spec)
     dt = time.perf_counter() - t0

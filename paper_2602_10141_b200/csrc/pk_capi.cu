@@ -12,7 +12,9 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -111,6 +113,19 @@ struct DevCtx {
   std::mutex mu;
   DBuf a, partials, groups, out, primes, starts, lens, blockout, blockabs, modp_out;
   std::map<std::pair<const void*, int>, int> occ;  // (kernel, smem) -> CTAs per SM
+  // per-matrix batched walks: launches round-robin over kAux streams so each
+  // launch's tail overlaps the next launch (created on first use)
+  static constexpr int kAux = 4;
+  cudaStream_t aux[kAux] = {};
+  cudaEvent_t ev_main = nullptr, ev_aux[kAux] = {};
+  void ensure_aux() {
+    if (aux[0]) return;
+    for (int i = 0; i < kAux; ++i) {
+      PK_CUDA(cudaStreamCreateWithFlags(&aux[i], cudaStreamNonBlocking));
+      PK_CUDA(cudaEventCreateWithFlags(&ev_aux[i], cudaEventDisableTiming));
+    }
+    PK_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
+  }
 };
 
 static std::mutex g_ctx_mu;
@@ -199,6 +214,29 @@ static Plan make_plan(int n, int algo, int B) {
   p.group = std::max<uint64_t>(1, p.tiles_total / kMaxGroups);
   p.piece_bits = std::min(p.k, 10);
   return p;
+}
+
+// Batched walks with one single-matrix (column 0 in the parameter) launch per
+// matrix: <= 2^10 tiles per matrix, independent of the batch size.  Used when a
+// matrix is large enough (m >= kPerMatrixMinM) that a launch is a useful amount
+// of work; $PK_BATCH_PER_MATRIX=0/1 forces either mode (measurement).
+constexpr int kPerMatrixMinM = 22;
+static Plan make_plan_per_matrix(int n, int algo) {
+  Plan p = make_plan(n, algo, 1);
+  if (p.k == 0) return p;
+  const int kmin = std::min(p.m - kTileBits, 8);
+  p.k = std::max(kmin, p.m - kTileBits - 10);
+  p.tiles_total = 1ull << (p.m - p.k - kTileBits);
+  p.group = std::max<uint64_t>(1, p.tiles_total / kMaxGroups);
+  p.piece_bits = std::min(p.k, 10);
+  return p;
+}
+static bool batch_per_matrix(int m) {
+  static const int force = [] {
+    const char* e = std::getenv("PK_BATCH_PER_MATRIX");
+    return e && *e ? std::atoi(e) : -1;
+  }();
+  return force >= 0 ? force != 0 : m >= kPerMatrixMinM;
 }
 
 struct Range {
@@ -306,9 +344,10 @@ static F64Launch prepare_f64(DevCtx& c, const Plan& p, bool cplx, int algo, int 
   return L;
 }
 
-static void launch_walk(DevCtx& c, const void* fn, int grid, int smem, WalkArgs& args) {
+static void launch_walk(DevCtx& c, const void* fn, int grid, int smem, WalkArgs& args,
+                        cudaStream_t st = nullptr) {
   void* kargs[] = {&args};
-  PK_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kWalkThreads), kargs, smem, c.stream));
+  PK_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kWalkThreads), kargs, smem, st ? st : c.stream));
 }
 
 // Two-stage deterministic reduction of [B][nt] tile partials into [B][5]
@@ -621,7 +660,35 @@ extern "C" int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex,
       auto* d_a = static_cast<double*>(c.a.get(nb * mat * 8));
       PK_CUDA(cudaMemcpyAsync(d_a, a + b0 * mat, nb * mat * 8, cudaMemcpyHostToDevice, c.stream));
       std::vector<double> h(static_cast<size_t>(nb) * kPartialStride);
-      if (p.k > 0) {
+      if (p.k > 0 && batch_per_matrix(p.m)) {
+        // one C0P launch per matrix over the aux streams; sub-batches bound the
+        // partials buffer; one reduce per sub-batch on the main stream
+        const Plan p1 = make_plan_per_matrix(n, algo);
+        const uint64_t nt = p1.tiles_total;
+        c.ensure_aux();
+        const int sb = static_cast<int>(std::clamp<uint64_t>((1ull << 24) / (nt * kPartialStride), 1, nb));
+        auto* d_part = static_cast<double*>(c.partials.get(sb * nt * kPartialStride * 8));
+        auto* d_out = static_cast<double*>(c.out.get(nb * kPartialStride * 8));
+        auto* d_grp = static_cast<double*>(c.groups.get(group_scratch_doubles(sb, nt, p1.group) * 8));
+        for (int s0 = 0; s0 < nb; s0 += sb) {
+          const int ns = std::min(sb, nb - s0);
+          PK_CUDA(cudaEventRecord(c.ev_main, c.stream));  // input copied, previous reduce done
+          for (int i = 0; i < DevCtx::kAux; ++i) PK_CUDA(cudaStreamWaitEvent(c.aux[i], c.ev_main, 0));
+          for (int b = 0; b < ns; ++b) {
+            const size_t off = static_cast<size_t>(s0 + b) * mat;
+            F64Launch L = prepare_f64(c, p1, cplx, algo, 1, d_a + off, 0, nt, abs_sums != nullptr,
+                                      d_part + b * nt * kPartialStride, a + b0 * mat + off);
+            launch_walk(c, L.fn, L.grid, L.smem, L.args, c.aux[b % DevCtx::kAux]);
+          }
+          for (int i = 0; i < DevCtx::kAux; ++i) {
+            PK_CUDA(cudaEventRecord(c.ev_aux[i], c.aux[i]));
+            PK_CUDA(cudaStreamWaitEvent(c.stream, c.ev_aux[i], 0));
+          }
+          launch_reduce(c, d_part, ns, 0, nt, p1.group, d_grp, d_out + s0 * kPartialStride);
+        }
+        PK_CUDA(cudaMemcpyAsync(h.data(), d_out, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+        PK_CUDA(cudaStreamSynchronize(c.stream));
+      } else if (p.k > 0) {
         const uint64_t nt = p.tiles_total;
         auto* d_part = static_cast<double*>(c.partials.get(nb * nt * kPartialStride * 8));
         auto* d_out = static_cast<double*>(c.out.get(nb * kPartialStride * 8));
