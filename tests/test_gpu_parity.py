@@ -177,6 +177,29 @@ def test_batch_matches_single_calls(gpu):
     assert real.dtype == np.float64
 
 
+def test_batch_per_matrix_launches(gpu):
+    """m >= 22: perm_batch issues one column-0-in-parameter launch per matrix over
+    four streams (pk_capi.cu, batch_per_matrix).  At m = 23 its plan (2^10 tiles of
+    2^8-step segments) is the single-call plan, so the results are bit-identical to
+    pk_ryser_f64 over [0, 2^m); at m = 25 the segments differ (2^10 vs 2^8 steps) and
+    the two agree within the S-scaled bound."""
+    for kind, n, method in (("haar-u", 23, "ryser"), ("haar-u", 24, "glynn"),
+                            ("haar-o", 23, "ryser"), ("haar-u", 25, "ryser")):
+        m = n if method == "ryser" else n - 1
+        mats = ensembles.sample_batch(ensembles.EnsembleSpec(kind, n, 5, 2602), 0, 5)
+        raw, ab = perm_batch(mats, method=method, want_abs=True)
+        for i in (0, 3, 4):
+            s, c, a1 = gpu.ryser_f64(mats[i], method, 0, 1 << m, want_abs=True)
+            one = s + c
+            if method == "glynn":
+                one = one * 2.0 ** (1 - n)
+            if m == 23:
+                assert bits_equal(raw[i], one), (kind, n, method, i)
+            else:
+                assert abs(raw[i] - one) <= 4 * n * U * a1 + 4 * U * abs(one), (kind, n, i)
+        assert np.all(ab > 0)
+
+
 def test_sample_permanents_c1_vs_reference(gpu):
     g = load_golden("samplers.json")
     spec = ensembles.EnsembleSpec("haar-u", 20, 16, 2602)
