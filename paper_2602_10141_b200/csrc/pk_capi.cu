@@ -115,7 +115,7 @@ struct DevCtx {
   std::map<std::pair<const void*, int>, int> occ;  // (kernel, smem) -> CTAs per SM
   // per-matrix batched walks: launches round-robin over kAux streams so each
   // launch's tail overlaps the next launch (created on first use)
-  static constexpr int kAux = 4;
+  static constexpr int kAux = 8;
   cudaStream_t aux[kAux] = {};
   cudaEvent_t ev_main = nullptr, ev_aux[kAux] = {};
   void ensure_aux() {
@@ -231,12 +231,18 @@ static Plan make_plan_per_matrix(int n, int algo) {
   p.piece_bits = std::min(p.k, 10);
   return p;
 }
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
 static bool batch_per_matrix(int m) {
-  static const int force = [] {
-    const char* e = std::getenv("PK_BATCH_PER_MATRIX");
-    return e && *e ? std::atoi(e) : -1;
-  }();
+  static const int force = env_int("PK_BATCH_PER_MATRIX", -1);
   return force >= 0 ? force != 0 : m >= kPerMatrixMinM;
+}
+// streams the per-matrix launches rotate over ($PK_BATCH_STREAMS, measurement)
+static int batch_streams() {
+  static const int ns = std::clamp(env_int("PK_BATCH_STREAMS", 4), 1, 8);
+  return ns;
 }
 
 struct Range {
@@ -673,14 +679,15 @@ extern "C" int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex,
         for (int s0 = 0; s0 < nb; s0 += sb) {
           const int ns = std::min(sb, nb - s0);
           PK_CUDA(cudaEventRecord(c.ev_main, c.stream));  // input copied, previous reduce done
-          for (int i = 0; i < DevCtx::kAux; ++i) PK_CUDA(cudaStreamWaitEvent(c.aux[i], c.ev_main, 0));
+          const int nst = batch_streams();
+          for (int i = 0; i < nst; ++i) PK_CUDA(cudaStreamWaitEvent(c.aux[i], c.ev_main, 0));
           for (int b = 0; b < ns; ++b) {
             const size_t off = static_cast<size_t>(s0 + b) * mat;
             F64Launch L = prepare_f64(c, p1, cplx, algo, 1, d_a + off, 0, nt, abs_sums != nullptr,
                                       d_part + b * nt * kPartialStride, a + b0 * mat + off);
-            launch_walk(c, L.fn, L.grid, L.smem, L.args, c.aux[b % DevCtx::kAux]);
+            launch_walk(c, L.fn, L.grid, L.smem, L.args, c.aux[b % nst]);
           }
-          for (int i = 0; i < DevCtx::kAux; ++i) {
+          for (int i = 0; i < nst; ++i) {
             PK_CUDA(cudaEventRecord(c.ev_aux[i], c.aux[i]));
             PK_CUDA(cudaStreamWaitEvent(c.stream, c.ev_aux[i], 0));
           }
