@@ -220,7 +220,7 @@ static Plan make_plan(int n, int algo, int B) {
 // matrix: <= 2^10 tiles per matrix, independent of the batch size.  Used when a
 // matrix is large enough (m >= kPerMatrixMinM) that a launch is a useful amount
 // of work; $PK_BATCH_PER_MATRIX=0/1 forces either mode (measurement).
-constexpr int kPerMatrixMinM = 22;
+constexpr int kPerMatrixMinM = 21;
 static Plan make_plan_per_matrix(int n, int algo) {
   Plan p = make_plan(n, algo, 1);
   if (p.k == 0) return p;
@@ -241,7 +241,7 @@ static bool batch_per_matrix(int m) {
 }
 // streams the per-matrix launches rotate over ($PK_BATCH_STREAMS, measurement)
 static int batch_streams() {
-  static const int ns = std::clamp(env_int("PK_BATCH_STREAMS", 4), 1, 8);
+  static const int ns = std::clamp(env_int("PK_BATCH_STREAMS", 8), 1, 8);
   return ns;
 }
 
