@@ -115,7 +115,7 @@ struct DevCtx {
   std::map<std::pair<const void*, int>, int> occ;  // (kernel, smem) -> CTAs per SM
   // per-matrix batched walks: launches round-robin over kAux streams so each
   // launch's tail overlaps the next launch (created on first use)
-  static constexpr int kAux = 8;
+  static constexpr int kAux = 16;
   cudaStream_t aux[kAux] = {};
   cudaEvent_t ev_main = nullptr, ev_aux[kAux] = {};
   void ensure_aux() {
@@ -220,7 +220,9 @@ static Plan make_plan(int n, int algo, int B) {
 // matrix: <= 2^10 tiles per matrix, independent of the batch size.  Used when a
 // matrix is large enough (m >= kPerMatrixMinM) that a launch is a useful amount
 // of work; $PK_BATCH_PER_MATRIX=0/1 forces either mode (measurement).
-constexpr int kPerMatrixMinM = 21;
+// complex launches are ~3x longer than real ones at the same m (6 vs 2 FP64
+// instructions per row update), so real walks switch later
+constexpr int kPerMatrixMinM = 20, kPerMatrixMinMReal = 21;
 static Plan make_plan_per_matrix(int n, int algo) {
   Plan p = make_plan(n, algo, 1);
   if (p.k == 0) return p;
@@ -235,13 +237,13 @@ static int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : dflt;
 }
-static bool batch_per_matrix(int m) {
+static bool batch_per_matrix(int m, bool cplx) {
   static const int force = env_int("PK_BATCH_PER_MATRIX", -1);
-  return force >= 0 ? force != 0 : m >= kPerMatrixMinM;
+  return force >= 0 ? force != 0 : m >= (cplx ? kPerMatrixMinM : kPerMatrixMinMReal);
 }
 // streams the per-matrix launches rotate over ($PK_BATCH_STREAMS, measurement)
 static int batch_streams() {
-  static const int ns = std::clamp(env_int("PK_BATCH_STREAMS", 8), 1, 8);
+  static const int ns = std::clamp(env_int("PK_BATCH_STREAMS", 16), 1, DevCtx::kAux);
   return ns;
 }
 
@@ -666,7 +668,7 @@ extern "C" int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex,
       auto* d_a = static_cast<double*>(c.a.get(nb * mat * 8));
       PK_CUDA(cudaMemcpyAsync(d_a, a + b0 * mat, nb * mat * 8, cudaMemcpyHostToDevice, c.stream));
       std::vector<double> h(static_cast<size_t>(nb) * kPartialStride);
-      if (p.k > 0 && batch_per_matrix(p.m)) {
+      if (p.k > 0 && batch_per_matrix(p.m, cplx)) {
         // one C0P launch per matrix over the aux streams; sub-batches bound the
         // partials buffer; one reduce per sub-batch on the main stream
         const Plan p1 = make_plan_per_matrix(n, algo);

@@ -178,13 +178,15 @@ def test_batch_matches_single_calls(gpu):
 
 
 def test_batch_per_matrix_launches(gpu):
-    """m >= 21: perm_batch issues one column-0-in-parameter launch per matrix over
-    eight streams (pk_capi.cu, batch_per_matrix).  At m = 23 its plan (2^10 tiles of
-    2^8-step segments) is the single-call plan, so the results are bit-identical to
-    pk_ryser_f64 over [0, 2^m); at m = 25 the segments differ (2^10 vs 2^8 steps) and
-    the two agree within the S-scaled bound."""
-    for kind, n, method in (("haar-u", 21, "ryser"), ("haar-u", 23, "ryser"), ("haar-u", 24, "glynn"),
-                            ("haar-o", 23, "ryser"), ("haar-u", 25, "ryser")):
+    """m >= 20 (complex; real m >= 21): perm_batch issues one column-0-in-parameter
+    launch per matrix over sixteen streams (pk_capi.cu, batch_per_matrix).  At m = 23
+    its plan (2^10 tiles of 2^8-step segments) is the single-call plan, so the results
+    are bit-identical to pk_ryser_f64 over [0, 2^m); at other m the segments differ
+    (e.g. 2^10 vs 2^8 steps at m = 25) and the two agree within the S-scaled bound."""
+    for kind, n, method in (("haar-u", 20, "ryser"), ("haar-u", 21, "glynn"),
+                            ("haar-u", 23, "ryser"), ("haar-u", 24, "glynn"),
+                            ("haar-o", 21, "ryser"), ("haar-o", 23, "ryser"),
+                            ("haar-u", 25, "ryser")):
         m = n if method == "ryser" else n - 1
         mats = ensembles.sample_batch(ensembles.EnsembleSpec(kind, n, 5, 2602), 0, 5)
         raw, ab = perm_batch(mats, method=method, want_abs=True)
