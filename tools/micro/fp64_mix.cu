@@ -53,7 +53,45 @@ void run(int ctas_per_sm) {
          MODE ? "chain" : "tree", ctas_per_sm, fa.numRegs, ops / (ms * 1e-3), 100 * ops / (ms * 1e-3) / 1.78e13);
   cudaFree(o);
 }
+// real walk mix: DFMA update + DMUL tree, H real rows per thread
+template <int H>
+__global__ void __launch_bounds__(128) kr(int iters, double* out, double sgv) {
+  double r[H], c[H];
+  for (int j = 0; j < H; ++j) {
+    r[j] = 0.9 + 0.001 * j + threadIdx.x * 1e-6;
+    c[j] = 1e-3 * j;
+  }
+  double s = 0;
+  for (int it = 0; it < iters; ++it) {
+    double sg = (it & 1) ? -sgv : sgv;
+    for (int j = 0; j < H; ++j) r[j] = fma(sg, c[j], r[j]);
+    double t[H];
+    for (int j = 0; j < H; ++j) t[j] = r[j];
+    for (int w = 1; w < H; w *= 2)
+      for (int i = 0; i + w < H; i += 2 * w) t[i] *= t[i + w];
+    s += t[0];
+  }
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+template <int H>
+void runr(int ctas_per_sm) {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  double* o; cudaMalloc(&o, 1024 * 8);
+  int iters = 40000;
+  kr<H><<<sms * ctas_per_sm, 128>>>(100, o, 1e-9);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  cudaEventRecord(a);
+  kr<H><<<sms * ctas_per_sm, 128>>>(iters, o, 1e-9);
+  cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  double ops = (2.0 * H) * iters * 128.0 * sms * ctas_per_sm;
+  cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kr<H>);
+  printf("real H=%d ctas/sm=%d regs=%d: %.3e fp64 lane-ops/s (%.1f%% of 1.78e13)\n", H, ctas_per_sm,
+         fa.numRegs, ops / (ms * 1e-3), 100 * ops / (ms * 1e-3) / 1.78e13);
+  cudaFree(o);
+}
 int main() {
+  runr<32>(2); runr<32>(3); runr<32>(4);
   run<16, 0>(1); run<16, 0>(2); run<16, 0>(3); run<16, 0>(4);
   run<16, 1>(2); run<16, 1>(3); run<16, 1>(4);
   run<8, 0>(4); run<8, 0>(8);
