@@ -89,7 +89,10 @@ int pk_ryser_f64_blocks(const double* a, int n, int is_complex, int algo,
  * Full-range permanents of B matrices (contiguous B x n x n), e.g. the
  * ensemble sampler (ensembles.py:142-158) and the geodesic sweep
  * (geodesics.py:153-179).  out[4*b ..] as in pk_ryser_f64 for matrix b;
- * abs_sums[b] optional.  Matrices are split over ndev devices.
+ * abs_sums[b] optional.  Matrices are split over ndev devices.  On each
+ * device, m >= 20 (complex) or m >= 21 (real) runs one launch per matrix
+ * over 16 streams; smaller m runs one matrix per warp in a single launch.
+ * Either way the call returns only after every result is on the host.
  */
 int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex, int algo, int ndev,
                        double* out, double* abs_sums);
