@@ -49,6 +49,13 @@ int pk_device_count(void);
  * Default 0.  Returns 0 or PK_ERR_ARG. */
 int pk_set_device_base(int base);
 
+/* Test / measurement hook (also $PK_LOGICAL_DEVICES): report `count` devices
+ * and map logical device d onto visible GPU d mod (visible GPUs), each with its
+ * own stream, buffers and host thread, so every multi-device path (range and
+ * modulus splits, the combine of device results) runs on a one-GPU box as on
+ * eight.  0 = off (default).  Returns 0 or PK_ERR_ARG. */
+int pk_set_logical_devices(int count);
+
 /* Library version, e.g. 100 for 0.1.0. */
 int pk_version(void);
 
@@ -68,8 +75,9 @@ int pk_max_n(void);
  *   ndev    = devices to split the range over (clamped to the device count).
  * The aligned interior runs in the register-resident production kernel; an
  * unaligned head/tail is walked with the reference's exact arithmetic.
- * The result for a given (a, start, length) is deterministic and, for
- * power-of-two ndev, identical for every ndev.
+ * The result for a given (a, start, length) is deterministic and identical
+ * for every ndev: devices own whole reduction groups and the host completes
+ * the group tree in global index order.
  */
 int pk_ryser_f64(const double* a, int n, int is_complex, int algo, uint64_t start,
                  uint64_t length, int ndev, double out[4], double* abs_sum);
@@ -92,7 +100,9 @@ int pk_ryser_f64_blocks(const double* a, int n, int is_complex, int algo,
  * abs_sums[b] optional.  Matrices are split over ndev devices.  On each
  * device, m >= 20 (complex) or m >= 21 (real) runs one launch per matrix
  * over 16 streams; smaller m runs one matrix per warp in a single launch.
- * Either way the call returns only after every result is on the host.
+ * Either way the call returns only after every result is on the host.  The
+ * walk plan depends on (n, algo) only, so results never depend on B, on the
+ * batch split over devices or on a caller's chunking.
  */
 int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex, int algo, int ndev,
                        double* out, double* abs_sums);
@@ -138,6 +148,14 @@ int pk_job_run(pk_job* job, int iters, size_t flush_bytes, double* total_ms, dou
 /* info[0..7] = k (segment bits), tiles, grid CTAs, CTAs per SM, registers per
  * thread, local (spill) bytes, dynamic smem bytes, kernel launches per run. */
 int pk_job_info(pk_job* job, int64_t* info);
+/* F_p jobs: per launch group g < min(G, max_groups) of the last pk_job_run,
+ * desc[6*g ..] = {kind (0 reduced, 1 lazy, 2 hybrid, 3 hybrid with a wide fp64
+ * prime, 4 Montgomery-64), primes in the group, registers per thread, CTAs
+ * per SM, grid CTAs, dynamic smem bytes} and ms[g] = summed device time of
+ * the group's walk launches (CUDA events on the job's stream).  prime_idx
+ * [4*g ..] = the group's indices into the job's prime list (-1 padded).
+ * Returns G (launch groups per run). */
+int pk_job_groups(pk_job* job, int64_t* desc, double* ms, int64_t* prime_idx, int max_groups);
 void pk_job_destroy(pk_job* job);
 
 /*

@@ -55,6 +55,7 @@ def _bind(lib):
         "pk_last_error": (ctypes.c_char_p, []),
         "pk_device_count": (_int, []),
         "pk_set_device_base": (_int, [_int]),
+        "pk_set_logical_devices": (_int, [_int]),
         "pk_version": (_int, []),
         "pk_max_n": (_int, []),
         "pk_ryser_f64": (_int, [_vp, _int, _int, _int, _u64, _u64, _int, P(_dbl), P(_dbl)]),
@@ -65,6 +66,7 @@ def _bind(lib):
         "pk_job_modp_create": (_int, [_int, _vp, _vp, _int, _int, _int, _u64, _u64, P(_vp)]),
         "pk_job_run": (_int, [_vp, _int, ctypes.c_size_t, P(_dbl), P(_dbl), _vp, _vp]),
         "pk_job_info": (_int, [_vp, _vp]),
+        "pk_job_groups": (_int, [_vp, _vp, _vp, _vp, _int]),
         "pk_job_destroy": (None, [_vp]),
         "pk_measure_peaks": (_int, [_int, _vp, _int]),
         "pk_peak_names": (ctypes.c_char_p, []),
@@ -81,9 +83,10 @@ def _bind(lib):
 def exported_symbols():
     """Names of the C-ABI entry points this binding requires."""
     return [
-        "pk_last_error", "pk_device_count", "pk_set_device_base", "pk_version", "pk_max_n", "pk_ryser_f64",
+        "pk_last_error", "pk_device_count", "pk_set_device_base", "pk_set_logical_devices",
+        "pk_version", "pk_max_n", "pk_ryser_f64",
         "pk_ryser_f64_blocks", "pk_ryser_f64_batch", "pk_ryser_modp", "pk_job_f64_create",
-        "pk_job_modp_create", "pk_job_run", "pk_job_info", "pk_job_destroy",
+        "pk_job_modp_create", "pk_job_run", "pk_job_info", "pk_job_groups", "pk_job_destroy",
         "pk_measure_peaks", "pk_peak_names", "pk_measure_latencies", "pk_latency_names",
     ]
 
@@ -126,6 +129,12 @@ def device_count() -> int:
 def set_device_base(base: int):
     """Logical device 0 of every call becomes physical device ``base`` (one process per GPU)."""
     _check(lib().pk_set_device_base(int(base)))
+
+
+def set_logical_devices(count: int):
+    """Test / measurement hook: report ``count`` devices, logical device d on
+    visible GPU d mod (visible GPUs); 0 turns it off (permkit_gpu.h)."""
+    _check(lib().pk_set_logical_devices(int(count)))
 
 
 def require_gpu():
@@ -256,6 +265,25 @@ class Job:
         _check(lib().pk_job_info(self._h, _ptr(buf)))
         keys = ["k", "tiles", "grid", "ctas_per_sm", "regs", "local_bytes", "smem", "launches"]
         return {k: int(v) for k, v in zip(keys, buf)}
+
+    GROUP_KINDS = ("reduced", "lazy", "hybrid", "hybrid_wide", "wide")
+
+    def groups(self) -> list:
+        """Per launch group of an F_p job: kind, primes (indices into the job's
+        prime list), launch shape and the walk ms of the last run()."""
+        desc = np.zeros((16, 6), dtype=np.int64)
+        ms = np.zeros(16, dtype=np.float64)
+        idx = np.zeros((16, 4), dtype=np.int64)
+        g = lib().pk_job_groups(self._h, _ptr(desc), _ptr(ms), _ptr(idx), 16)
+        if g < 0:
+            _check(g)
+        out = []
+        for i in range(min(g, 16)):
+            kind, P, regs, occ, grid, smem = (int(x) for x in desc[i])
+            out.append({"kind": self.GROUP_KINDS[kind], "P": P, "regs": regs, "ctas_per_sm": occ,
+                        "grid": grid, "smem": smem, "ms": float(ms[i]),
+                        "prime_idx": [int(x) for x in idx[i] if x >= 0]})
+        return out
 
     def close(self):
         if self._h:

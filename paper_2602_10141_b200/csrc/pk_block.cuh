@@ -50,16 +50,19 @@ __device__ __forceinline__ void neumaier_ref(double& s, double& c, double v) {
 
 __device__ __forceinline__ int ctz64(uint64_t x) { return __ffsll(static_cast<long long>(x)) - 1; }
 
-// out[blk * 4 + {0,1,2,3}] = (s_re, s_im, c_re, c_im)
+// out[blk * 4 + {0,1,2,3}] = (s_re, s_im, c_re, c_im); block blk walks matrix
+// a + (blk / ppm) * mat_stride (ppm = nblocks, stride 0: one matrix)
 template <bool CPLX, int ALGO>
 __global__ void __launch_bounds__(kBlockThreads) block_f64_kernel(const double* __restrict__ a,
                                                                   int n,
                                                                   const uint64_t* __restrict__ starts,
                                                                   const uint64_t* __restrict__ lens,
                                                                   int nblocks, double* out,
-                                                                  double* abs_out) {
+                                                                  double* abs_out, int ppm,
+                                                                  size_t mat_stride) {
   const int blk = blockIdx.x * blockDim.x + threadIdx.x;
   if (blk >= nblocks) return;
+  a += static_cast<size_t>(blk / ppm) * mat_stride;  // ppm blocks per matrix (batched pieces)
   C2 r[kBlockMaxN];
   double abs_acc = 0.0;
   auto A = [&](int i, int j) -> C2 {

@@ -131,7 +131,12 @@ struct DevCtx {
 static std::mutex g_ctx_mu;
 static DevCtx* g_ctx[64] = {};
 
-static int device_count() {
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
+static int physical_device_count() {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
@@ -142,27 +147,52 @@ static int device_count() {
   return n;
 }
 
-// Logical device d of every entry point is physical device base + d, so that
-// one process per GPU (torchrun) can address "its" GPU as device 0.
+// $PK_LOGICAL_DEVICES = L > 0 (test and measurement hook): the library reports
+// L devices and maps logical device d onto physical GPU d mod (visible GPUs),
+// each with its own context (stream, buffers, lock, host thread).  Every
+// multi-device code path -- the per-device host threads, the range and modulus
+// splits and the combine of the device results -- then runs on a one-GPU box
+// exactly as it does on eight GPUs (the devices never wait on each other).
+// pk_set_logical_devices() changes it at run time; a context, once created,
+// keeps its GPU, and logical d < (visible GPUs) is GPU d in both modes.
+static std::atomic<int> g_logical{-1};
+static int logical_devices() {
+  int L = g_logical.load();
+  if (L < 0) {
+    L = std::clamp(env_int("PK_LOGICAL_DEVICES", 0), 0, 64);
+    g_logical.store(L);
+  }
+  return L;
+}
+
+static int device_count() {
+  const int nd = physical_device_count();
+  return (nd > 0 && logical_devices() > 0) ? logical_devices() : nd;
+}
+
+// Logical device d of every entry point is device base + d, so that one
+// process per GPU (torchrun) can address "its" GPU as device 0.
 static std::atomic<int> g_device_base{0};
 
 static DevCtx& ctx(int logical) {
   std::lock_guard<std::mutex> g(g_ctx_mu);
-  const int dev = logical + g_device_base.load();
-  PK_REQUIRE(logical >= 0 && dev < 64, kErrArg, "device index out of range");
-  if (!g_ctx[dev]) {
+  const int idx = logical + g_device_base.load();
+  PK_REQUIRE(logical >= 0 && idx < 64, kErrArg, "device index out of range");
+  if (!g_ctx[idx]) {
+    const int nphys = physical_device_count();
     const int nd = device_count();
-    PK_REQUIRE(dev < nd, kErrArg,
-               "CUDA device " + std::to_string(dev) + " not available (" + std::to_string(nd) +
+    PK_REQUIRE(idx < nd, kErrArg,
+               "CUDA device " + std::to_string(idx) + " not available (" + std::to_string(nd) +
                    " visible)");
+    const int dev = logical_devices() > 0 ? idx % nphys : idx;
     auto* c = new DevCtx;
     c->dev = dev;
     PK_CUDA(cudaSetDevice(dev));
     PK_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
     PK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    g_ctx[dev] = c;
+    g_ctx[idx] = c;
   }
-  return *g_ctx[dev];
+  return *g_ctx[idx];
 }
 
 static int occupancy(DevCtx& c, const void* fn, int threads, int smem) {
@@ -190,9 +220,10 @@ struct Plan {
   int piece_bits = 10;       // ragged pieces are aligned to 2^piece_bits
 };
 
-static int ilog2_floor(double x) { return x < 1 ? 0 : static_cast<int>(std::floor(std::log2(x))); }
-
-static Plan make_plan(int n, int algo, int B) {
+// The plan depends on (n, algo) only -- never on a batch size, a device count
+// or a chunking -- so a matrix's fp64 bits are the same whichever call walks it
+// (single, batched, split over devices; reference engine.py:5-8).
+static Plan make_plan(int n, int algo) {
   Plan p;
   p.n = n;
   p.m = algo == PK_ALGO_RYSER ? n : n - 1;
@@ -202,14 +233,9 @@ static Plan make_plan(int n, int algo, int B) {
     p.piece_bits = std::max(m, 1);
     return p;
   }
-  // tiles of 2^kTileBits segments of 2^k indices; ~2^17 tiles per launch
+  // tiles of 2^kTileBits segments of 2^k indices; ~2^17 tiles per matrix
   const int kmin = std::min(m - kTileBits, 8);
-  if (B <= 1) {
-    p.k = std::max(kmin, m - kTileBits - 17);
-  } else {
-    const int t = std::clamp(ilog2_floor(double(1 << 17) / B), 0, m - kTileBits - kmin);
-    p.k = m - kTileBits - t;
-  }
+  p.k = std::max(kmin, m - kTileBits - 17);
   p.tiles_total = 1ull << (m - p.k - kTileBits);
   p.group = std::max<uint64_t>(1, p.tiles_total / kMaxGroups);
   p.piece_bits = std::min(p.k, 10);
@@ -224,7 +250,7 @@ static Plan make_plan(int n, int algo, int B) {
 // instructions per row update), so real walks switch later
 constexpr int kPerMatrixMinM = 20, kPerMatrixMinMReal = 21;
 static Plan make_plan_per_matrix(int n, int algo) {
-  Plan p = make_plan(n, algo, 1);
+  Plan p = make_plan(n, algo);
   if (p.k == 0) return p;
   const int kmin = std::min(p.m - kTileBits, 8);
   p.k = std::max(kmin, p.m - kTileBits - 10);
@@ -233,13 +259,15 @@ static Plan make_plan_per_matrix(int n, int algo) {
   p.piece_bits = std::min(p.k, 10);
   return p;
 }
-static int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e && *e ? std::atoi(e) : dflt;
-}
 static bool batch_per_matrix(int m, bool cplx) {
   static const int force = env_int("PK_BATCH_PER_MATRIX", -1);
   return force >= 0 ? force != 0 : m >= (cplx ? kPerMatrixMinM : kPerMatrixMinMReal);
+}
+// test hook: cap the matrices per sub-batch ($PK_BATCH_SUBBATCH) so small tests
+// exercise the sub-batch loops (buffer reuse across sub-batches)
+static int subbatch_cap(int sb) {
+  const int cap = env_int("PK_BATCH_SUBBATCH", 0);  // read per call (tests set it)
+  return cap > 0 ? std::min(sb, cap) : sb;
 }
 // streams the per-matrix launches rotate over ($PK_BATCH_STREAMS, measurement)
 static int batch_streams() {
@@ -366,24 +394,59 @@ static void launch_reduce(DevCtx& c, const double* d_partials, int B, uint64_t t
   const int ng = static_cast<int>(g1 - g0);
   PK_REQUIRE(g1 - g0 <= static_cast<uint64_t>(kMaxGroups) + 1, kErrInternal,
              "too many reduction groups");
-  dim3 fg((ng + kFoldThreads - 1) / kFoldThreads, B);
-  fold_groups_kernel<<<fg, kFoldThreads, 0, c.stream>>>(d_partials, t0, nt, group, g0, ng, d_groups);
-  PK_CUDA(cudaGetLastError());
+  // gridDim.y <= 65535: matrices in slices
+  for (int b0 = 0; b0 < B; b0 += 65535) {
+    const int nb = std::min(B - b0, 65535);
+    dim3 fg((ng + kFoldThreads - 1) / kFoldThreads, nb);
+    fold_groups_kernel<<<fg, kFoldThreads, 0, c.stream>>>(
+        d_partials + static_cast<size_t>(b0) * nt * kPartialStride, t0, nt, group, g0, ng,
+        d_groups + static_cast<size_t>(b0) * ng * kPartialStride);
+    PK_CUDA(cudaGetLastError());
+  }
+  if (d_out == nullptr) return;  // multi-device: the host completes the tree
   tree_groups_kernel<<<B, kTreeThreads, 0, c.stream>>>(d_groups, g0, ng, d_out);
   PK_CUDA(cudaGetLastError());
+}
+
+// Host copy of tree_groups_kernel (pk_reduce.cuh): the binary tree over group
+// nodes on GLOBAL indices g0 .. g0 + size - 1, a missing child passing its
+// sibling through.  With the groups of several devices concatenated in index
+// order it reproduces the one-device root bit for bit (pair_combine is
+// adds/subtracts only, so there is no contraction to differ).
+static Node tree_nodes_host(std::vector<Node> cur, uint64_t g0) {
+  uint64_t lo = g0, hi = g0 + cur.size() - 1;
+  while (lo != hi) {
+    const uint64_t nlo = lo >> 1, nhi = hi >> 1;
+    std::vector<Node> nxt;
+    nxt.reserve(nhi - nlo + 1);
+    for (uint64_t j = nlo; j <= nhi; ++j) {
+      const uint64_t l = 2 * j, r = 2 * j + 1;
+      const bool hl = l >= lo && l <= hi, hr = r >= lo && r <= hi;
+      if (hl && hr)
+        nxt.push_back(node_combine_h(cur[l - lo], cur[r - lo]));
+      else
+        nxt.push_back(hl ? cur[l - lo] : cur[r - lo]);
+    }
+    cur.swap(nxt);
+    lo = nlo;
+    hi = nhi;
+  }
+  return cur[0];
 }
 
 static size_t group_scratch_doubles(int B, uint64_t nt, uint64_t group) {
   return static_cast<size_t>(B) * (nt / group + 2) * kPartialStride;
 }
 
-// exact-arithmetic pieces on one device; returns one Node per piece
+// exact-arithmetic pieces on one device; returns one Node per piece.  Piece i
+// walks matrix d_a + (i / ppm) * mat_stride (default: every piece, one matrix).
 static std::vector<Node> run_f64_pieces(DevCtx& c, const double* d_a, int n, bool cplx, int algo,
                                         const std::vector<std::pair<uint64_t, uint64_t>>& pieces,
-                                        bool want_abs) {
+                                        bool want_abs, int ppm = 0, size_t mat_stride = 0) {
   std::vector<Node> res(pieces.size());
   if (pieces.empty()) return res;
   const int np = static_cast<int>(pieces.size());
+  if (ppm <= 0) ppm = np;
   std::vector<uint64_t> hs(np), hl(np);
   for (int i = 0; i < np; ++i) {
     hs[i] = pieces[i].first;
@@ -397,17 +460,20 @@ static std::vector<Node> run_f64_pieces(DevCtx& c, const double* d_a, int n, boo
   PK_CUDA(cudaMemcpyAsync(dl, hl.data(), np * 8, cudaMemcpyHostToDevice, c.stream));
   const int grid = (np + kBlockThreads - 1) / kBlockThreads;
   double* ab = want_abs ? dabs : nullptr;
+#define PK_BLOCK(C, A) \
+  block_f64_kernel<C, A><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab, ppm, mat_stride)
   if (cplx) {
     if (algo == 0)
-      block_f64_kernel<true, 0><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab);
+      PK_BLOCK(true, 0);
     else
-      block_f64_kernel<true, 1><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab);
+      PK_BLOCK(true, 1);
   } else {
     if (algo == 0)
-      block_f64_kernel<false, 0><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab);
+      PK_BLOCK(false, 0);
     else
-      block_f64_kernel<false, 1><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab);
+      PK_BLOCK(false, 1);
   }
+#undef PK_BLOCK
   PK_CUDA(cudaGetLastError());
   std::vector<double> h(np * 4), habs(np, 0.0);
   PK_CUDA(cudaMemcpyAsync(h.data(), dout, np * 4 * 8, cudaMemcpyDeviceToHost, c.stream));
@@ -451,23 +517,6 @@ static int clamp_ndev(int ndev) {
   const int nd = device_count() - g_device_base.load();
   PK_REQUIRE(nd > 0, kErrCuda, "no CUDA device visible");
   return std::max(1, std::min(ndev, nd));
-}
-
-// Binary tree over device roots (power-of-two count), else ordered fold.
-static Node combine_roots(const std::vector<Node>& v) {
-  std::vector<Node> cur = v;
-  const size_t n = cur.size();
-  if (n && (n & (n - 1)) == 0) {
-    while (cur.size() > 1) {
-      std::vector<Node> nxt;
-      for (size_t i = 0; i + 1 < cur.size(); i += 2) nxt.push_back(node_combine_h(cur[i], cur[i + 1]));
-      cur.swap(nxt);
-    }
-    return cur[0];
-  }
-  Node acc = cur[0];
-  for (size_t i = 1; i < n; ++i) acc = node_combine_h(acc, cur[i]);
-  return acc;
 }
 
 static void check_f64_args(const double* a, int n, int algo) {
@@ -530,6 +579,14 @@ extern "C" int pk_device_count(void) {
   return pk_guard([&]() -> int { return device_count(); });
 }
 
+extern "C" int pk_set_logical_devices(int count) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(count >= 0 && count <= 64, kErrArg, "logical device count must be in [0, 64]");
+    g_logical.store(count);
+    return 0;
+  });
+}
+
 extern "C" int pk_set_device_base(int base) {
   return pk_guard([&]() -> int {
     const int nd = device_count();
@@ -543,26 +600,36 @@ extern "C" int pk_set_device_base(int base) {
 
 namespace pk {
 
-// fp64 range on ndev devices
+// fp64 range on ndev devices.
+//
+// One device: walk + fold + tree on the device, one root.  Several devices: the
+// aligned tile interior is cut at reduction-group boundaries, each device walks
+// its share and folds its groups, and the host runs the group tree over all
+// devices' groups in global order (tree_nodes_host) -- bit-identical to one
+// device for ANY cut, aligned or not.  The ragged head / tail pieces (exact
+// kernel) are dealt round-robin over the devices and folded in index order.
 static Node f64_range(const double* a, int n, bool cplx, int algo, uint64_t start,
                       uint64_t length, int ndev, bool want_abs) {
   check_f64_args(a, n, algo);
-  const Plan p = make_plan(n, algo, 1);
+  const Plan p = make_plan(n, algo);
   check_range(p.m, start, length);
   const Range r = make_range(p, start, length);
   const size_t abytes = static_cast<size_t>(n) * n * (cplx ? 16 : 8);
   const uint64_t nt = r.t1 - r.t0;
-  ndev = nt ? clamp_ndev(ndev) : 1;
-  // split tiles on group boundaries
+  std::vector<std::pair<uint64_t, uint64_t>> pcs = r.head;
+  pcs.insert(pcs.end(), r.tail.begin(), r.tail.end());
+  ndev = (nt || pcs.size() > 1) ? clamp_ndev(ndev) : 1;
+  // interior cut on group boundaries (groups never straddle devices)
   std::vector<uint64_t> cut(ndev + 1);
   for (int d = 0; d <= ndev; ++d) {
     uint64_t t = r.t0 + nt * d / ndev;
     if (d > 0 && d < ndev) t = std::max(r.t0, std::min(r.t1, (t + p.group / 2) / p.group * p.group));
     cut[d] = t;
   }
-  std::vector<Node> roots(ndev);
-  std::vector<char> has(ndev, 0);
-  std::vector<Node> head, tail;
+  Node root{};
+  std::vector<std::vector<Node>> dev_groups(ndev);
+  std::vector<uint64_t> dev_g0(ndev, 0);
+  std::vector<Node> pres(pcs.size());
   for_devices(ndev, [&](int d) {
     DevCtx& c = ctx(d);
     std::lock_guard<std::mutex> g(c.mu);
@@ -572,28 +639,47 @@ static Node f64_range(const double* a, int n, bool cplx, int algo, uint64_t star
     const uint64_t t0 = cut[d], t1 = cut[d + 1];
     if (t1 > t0) {
       auto* d_part = static_cast<double*>(c.partials.get((t1 - t0) * kPartialStride * 8));
-      auto* d_out = static_cast<double*>(c.out.get(kPartialStride * 8));
       F64Launch L = prepare_f64(c, p, cplx, algo, 1, d_a, t0, t1 - t0, want_abs, d_part, a);
       launch_walk(c, L.fn, L.grid, L.smem, L.args);
       auto* d_grp = static_cast<double*>(c.groups.get(group_scratch_doubles(1, t1 - t0, p.group) * 8));
-      launch_reduce(c, d_part, 1, t0, t1 - t0, p.group, d_grp, d_out);
-      double h[kPartialStride];
-      PK_CUDA(cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-      PK_CUDA(cudaStreamSynchronize(c.stream));
-      roots[d] = node_from5(h);
-      has[d] = 1;
+      if (ndev == 1) {
+        auto* d_out = static_cast<double*>(c.out.get(kPartialStride * 8));
+        launch_reduce(c, d_part, 1, t0, t1 - t0, p.group, d_grp, d_out);
+        double h[kPartialStride];
+        PK_CUDA(cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+        PK_CUDA(cudaStreamSynchronize(c.stream));
+        root = node_from5(h);
+      } else {
+        launch_reduce(c, d_part, 1, t0, t1 - t0, p.group, d_grp, nullptr);
+        const uint64_t g0 = t0 / p.group, g1 = (t1 - 1) / p.group + 1;
+        std::vector<double> h((g1 - g0) * kPartialStride);
+        PK_CUDA(cudaMemcpyAsync(h.data(), d_grp, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+        PK_CUDA(cudaStreamSynchronize(c.stream));
+        dev_g0[d] = g0;
+        for (uint64_t gi = 0; gi < g1 - g0; ++gi) dev_groups[d].push_back(node_from5(&h[gi * kPartialStride]));
+      }
     }
-    if (d == 0) {
-      head = run_f64_pieces(c, d_a, n, cplx, algo, r.head, want_abs);
-      tail = run_f64_pieces(c, d_a, n, cplx, algo, r.tail, want_abs);
-    }
+    std::vector<std::pair<uint64_t, uint64_t>> mine;
+    for (size_t i = d; i < pcs.size(); i += ndev) mine.push_back(pcs[i]);
+    const std::vector<Node> v = run_f64_pieces(c, d_a, n, cplx, algo, mine, want_abs);
+    for (size_t i = d, j = 0; i < pcs.size(); i += ndev, ++j) pres[i] = v[j];
   });
-  std::vector<Node> rr;
-  for (int d = 0; d < ndev; ++d)
-    if (has[d]) rr.push_back(roots[d]);
-  std::vector<Node> seq = head;
-  if (!rr.empty()) seq.push_back(combine_roots(rr));
-  seq.insert(seq.end(), tail.begin(), tail.end());
+  if (ndev > 1 && nt) {
+    std::vector<Node> all;
+    uint64_t g0 = 0;
+    bool first = true;
+    for (int d = 0; d < ndev; ++d) {
+      if (dev_groups[d].empty()) continue;
+      if (first) g0 = dev_g0[d];
+      first = false;
+      all.insert(all.end(), dev_groups[d].begin(), dev_groups[d].end());
+    }
+    root = tree_nodes_host(std::move(all), g0);
+  }
+  // index order: head pieces, the interior root, tail pieces
+  std::vector<Node> seq(pres.begin(), pres.begin() + r.head.size());
+  if (nt) seq.push_back(root);
+  seq.insert(seq.end(), pres.begin() + r.head.size(), pres.end());
   if (seq.empty()) return Node{};
   Node acc = seq[0];
   for (size_t i = 1; i < seq.size(); ++i) acc = node_combine_h(acc, seq[i]);
@@ -664,7 +750,7 @@ extern "C" int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex,
       DevCtx& c = ctx(d);
       std::lock_guard<std::mutex> g(c.mu);
       PK_CUDA(cudaSetDevice(c.dev));
-      const Plan p = make_plan(n, algo, nb);
+      const Plan p = make_plan(n, algo);
       auto* d_a = static_cast<double*>(c.a.get(nb * mat * 8));
       PK_CUDA(cudaMemcpyAsync(d_a, a + b0 * mat, nb * mat * 8, cudaMemcpyHostToDevice, c.stream));
       std::vector<double> h(static_cast<size_t>(nb) * kPartialStride);
@@ -674,7 +760,8 @@ extern "C" int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex,
         const Plan p1 = make_plan_per_matrix(n, algo);
         const uint64_t nt = p1.tiles_total;
         c.ensure_aux();
-        const int sb = static_cast<int>(std::clamp<uint64_t>((1ull << 24) / (nt * kPartialStride), 1, nb));
+        const int sb = subbatch_cap(
+            static_cast<int>(std::clamp<uint64_t>((1ull << 24) / (nt * kPartialStride), 1, nb)));
         auto* d_part = static_cast<double*>(c.partials.get(sb * nt * kPartialStride * 8));
         auto* d_out = static_cast<double*>(c.out.get(nb * kPartialStride * 8));
         auto* d_grp = static_cast<double*>(c.groups.get(group_scratch_doubles(sb, nt, p1.group) * 8));
@@ -698,23 +785,29 @@ extern "C" int pk_ryser_f64_batch(const double* a, int B, int n, int is_complex,
         PK_CUDA(cudaMemcpyAsync(h.data(), d_out, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
         PK_CUDA(cudaStreamSynchronize(c.stream));
       } else if (p.k > 0) {
+        // a matrix per warp slot; sub-batches of <= 2^17 tiles bound the partials
         const uint64_t nt = p.tiles_total;
-        auto* d_part = static_cast<double*>(c.partials.get(nb * nt * kPartialStride * 8));
+        const int sb = subbatch_cap(static_cast<int>(std::clamp<uint64_t>((1ull << 17) / nt, 1, nb)));
+        auto* d_part = static_cast<double*>(c.partials.get(sb * nt * kPartialStride * 8));
         auto* d_out = static_cast<double*>(c.out.get(nb * kPartialStride * 8));
-        F64Launch L = prepare_f64(c, p, cplx, algo, nb, d_a, 0, nt, abs_sums != nullptr, d_part,
-                                  a + b0 * mat);
-        launch_walk(c, L.fn, L.grid, L.smem, L.args);
-        auto* d_grp = static_cast<double*>(c.groups.get(group_scratch_doubles(nb, nt, p.group) * 8));
-        launch_reduce(c, d_part, nb, 0, nt, p.group, d_grp, d_out);
+        auto* d_grp = static_cast<double*>(c.groups.get(group_scratch_doubles(sb, nt, p.group) * 8));
+        for (int s0 = 0; s0 < nb; s0 += sb) {
+          const int ns = std::min(sb, nb - s0);
+          const size_t off = static_cast<size_t>(s0) * mat;
+          F64Launch L = prepare_f64(c, p, cplx, algo, ns, d_a + off, 0, nt, abs_sums != nullptr,
+                                    d_part, a + b0 * mat + off);
+          launch_walk(c, L.fn, L.grid, L.smem, L.args);
+          launch_reduce(c, d_part, ns, 0, nt, p.group, d_grp, d_out + s0 * kPartialStride);
+        }
         PK_CUDA(cudaMemcpyAsync(h.data(), d_out, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
         PK_CUDA(cudaStreamSynchronize(c.stream));
       } else {
-        // tiny m: one exact piece per matrix (2^m <= 32 terms)
+        // tiny m: one exact piece per matrix (2^m <= 32 terms), all in one launch
+        std::vector<std::pair<uint64_t, uint64_t>> pcs(nb, {0, 1ull << p.m});
+        const std::vector<Node> v =
+            run_f64_pieces(c, d_a, n, cplx, algo, pcs, abs_sums != nullptr, 1, mat);
         for (int b = 0; b < nb; ++b) {
-          std::vector<std::pair<uint64_t, uint64_t>> pc{{0, 1ull << p.m}};
-          const std::vector<Node> v =
-              run_f64_pieces(c, d_a + b * mat, n, cplx, algo, pc, abs_sums != nullptr);
-          const Node& x = v[0];
+          const Node& x = v[b];
           double* o = h.data() + b * kPartialStride;
           o[0] = x.re.s;
           o[1] = x.re.c;
@@ -993,7 +1086,7 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
       for (size_t e = 0; e < nn; ++e)
         PK_REQUIRE(a[k * nn + e] < primes[k], kErrArg, "matrix residues must lie in [0, p)");
     }
-    const Plan p = make_plan(n, algo, 1);
+    const Plan p = make_plan(n, algo);
     check_range(p.m, start, length);
     const Range r = make_range(p, start, length);
     const uint64_t nt = r.t1 - r.t0;
@@ -1006,7 +1099,7 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
     }
     std::vector<uint64_t> res(P, 0);
     const std::vector<ModpGroup> gs = group_primes(fast, primes, n);
-    ndev = (nt && !gs.empty()) ? clamp_ndev(ndev) : 1;
+    ndev = clamp_ndev(ndev);
     std::vector<uint64_t> cut(ndev + 1);
     for (int d = 0; d <= ndev; ++d) cut[d] = r.t0 + nt * d / ndev;
     std::vector<std::vector<uint64_t>> dev_res(ndev, std::vector<uint64_t>(P, 0));
@@ -1032,24 +1125,27 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
         PK_CUDA(cudaStreamSynchronize(c.stream));
         decode_group(G, ho.data(), primes, n, algo, dev_res[d].data());
       }
-      if (d == 0) {
-        // ragged head/tail of fast primes, and every slow modulus, on device 0
-        auto* d_a = static_cast<uint64_t*>(c.a.get(nn * 8));
-        for (int k = 0; k < P; ++k) {
-          const bool is_fast = std::find(fast.begin(), fast.end(), k) != fast.end();
-          std::vector<std::pair<uint64_t, uint64_t>> pcs;
-          if (is_fast) {
-            pcs = r.head;
-            pcs.insert(pcs.end(), r.tail.begin(), r.tail.end());
-          } else {
-            const int bits = std::clamp(p.m - 17, 6, 62);
-            split_pieces(start, start + length, bits, pcs);
-          }
-          if (pcs.empty()) continue;
-          PK_CUDA(cudaMemcpyAsync(d_a, a + k * nn, nn * 8, cudaMemcpyHostToDevice, c.stream));
-          const uint64_t v = modp_pieces(c, d_a, n, algo, primes[k], pcs);
-          dev_res[0][k] = static_cast<uint64_t>((static_cast<u128>(dev_res[0][k]) + v) % primes[k]);
+      // exact-kernel work, spread over the devices: the ragged head / tail
+      // pieces of the fast primes round-robin, and every slow modulus (even,
+      // composite or n > kMaxN) split into one contiguous share per device
+      std::vector<std::pair<uint64_t, uint64_t>> ragged = r.head;
+      ragged.insert(ragged.end(), r.tail.begin(), r.tail.end());
+      auto* d_a = static_cast<uint64_t*>(c.a.get(nn * 8));
+      for (int k = 0; k < P; ++k) {
+        const bool is_fast = std::find(fast.begin(), fast.end(), k) != fast.end();
+        std::vector<std::pair<uint64_t, uint64_t>> pcs;
+        if (is_fast) {
+          for (size_t i = d; i < ragged.size(); i += ndev) pcs.push_back(ragged[i]);
+        } else {
+          const uint64_t s0 = start + static_cast<uint64_t>(static_cast<u128>(length) * d / ndev);
+          const uint64_t s1 = start + static_cast<uint64_t>(static_cast<u128>(length) * (d + 1) / ndev);
+          const int bits = std::clamp(p.m - 17, 6, 62);
+          split_pieces(s0, s1, bits, pcs);
         }
+        if (pcs.empty()) continue;
+        PK_CUDA(cudaMemcpyAsync(d_a, a + k * nn, nn * 8, cudaMemcpyHostToDevice, c.stream));
+        const uint64_t v = modp_pieces(c, d_a, n, algo, primes[k], pcs);
+        dev_res[d][k] = static_cast<uint64_t>((static_cast<u128>(dev_res[d][k]) + v) % primes[k]);
       }
     });
     for (int k = 0; k < P; ++k) {
@@ -1086,6 +1182,7 @@ struct pk_job {
   std::vector<ModpLaunch> groups;  // F_p jobs: one launch per prime group
   std::vector<ModpGroup> gdesc;    // ... and its description (output words per group)
   size_t out_words = 0;            // F_p: length of d_modp
+  std::vector<double> group_ms;    // F_p: per-group walk time of the last run
 };
 
 static void job_free(pk_job* j) {
@@ -1112,7 +1209,7 @@ extern "C" int pk_job_f64_create(int device, const double* a, int n, int is_comp
     DevCtx& c = *j->c;
     std::lock_guard<std::mutex> g(c.mu);
     PK_CUDA(cudaSetDevice(c.dev));
-    j->plan = make_plan(n, algo, 1);
+    j->plan = make_plan(n, algo);
     check_range(j->plan.m, start, length);
     const Range r = make_range(j->plan, start, length);
     PK_REQUIRE(r.head.empty() && r.tail.empty() && r.t1 > r.t0, kErrArg,
@@ -1158,7 +1255,7 @@ extern "C" int pk_job_modp_create(int device, const uint64_t* a, const uint64_t*
       fast.push_back(k);
     }
     const std::vector<ModpGroup> gs = group_primes(fast, primes, n);
-    j->plan = make_plan(n, algo, 1);
+    j->plan = make_plan(n, algo);
     check_range(j->plan.m, start, length);
     const Range r = make_range(j->plan, start, length);
     PK_REQUIRE(r.head.empty() && r.tail.empty() && r.t1 > r.t0, kErrArg,
@@ -1214,20 +1311,28 @@ extern "C" int pk_job_run(pk_job* j, int iters, size_t flush_bytes, double* tota
       PK_CUDA(cudaMalloc(&j->d_flush, flush_bytes));
       j->flush_cap = flush_bytes;
     }
-    std::vector<cudaEvent_t> ev(2 * iters + 2);
+    // ev[0], ev[1]: the whole sequence; then per iteration one event before
+    // each launch group and one after the last (F_p: G groups; f64: one)
+    const int G = j->kind == 1 ? static_cast<int>(j->groups.size()) : 1;
+    std::vector<cudaEvent_t> ev(2 + static_cast<size_t>(iters) * (G + 1));
     for (auto& e : ev) PK_CUDA(cudaEventCreate(&e));
+    auto gev = [&](int it, int g) { return ev[2 + static_cast<size_t>(it) * (G + 1) + g]; };
     const size_t nres = j->kind == 1 ? j->out_words : 0;
     PK_CUDA(cudaEventRecord(ev[0], c.stream));
     for (int it = 0; it < iters; ++it) {
       if (flush_bytes) PK_CUDA(cudaMemsetAsync(j->d_flush, it & 0xff, flush_bytes, c.stream));
       if (j->kind == 1) PK_CUDA(cudaMemsetAsync(j->d_modp, 0, nres * 8, c.stream));
-      PK_CUDA(cudaEventRecord(ev[2 + 2 * it], c.stream));
       if (j->kind == 0) {
+        PK_CUDA(cudaEventRecord(gev(it, 0), c.stream));
         launch_walk(c, j->fn, j->grid, j->smem, j->args);
       } else {
-        for (auto& L : j->groups) launch_walk(c, L.fn, L.grid, L.smem, L.args);
+        for (int g = 0; g < G; ++g) {
+          PK_CUDA(cudaEventRecord(gev(it, g), c.stream));
+          auto& L = j->groups[g];
+          launch_walk(c, L.fn, L.grid, L.smem, L.args);
+        }
       }
-      PK_CUDA(cudaEventRecord(ev[3 + 2 * it], c.stream));
+      PK_CUDA(cudaEventRecord(gev(it, G), c.stream));
       if (j->kind == 0)
         launch_reduce(c, j->d_part, 1, j->t0, j->nt, j->plan.group, j->d_groups, j->d_out);
     }
@@ -1237,9 +1342,13 @@ extern "C" int pk_job_run(pk_job* j, int iters, size_t flush_bytes, double* tota
     PK_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
     if (total_ms) *total_ms = ms;
     double wsum = 0;
+    j->group_ms.assign(G, 0.0);
     for (int it = 0; it < iters; ++it) {
-      PK_CUDA(cudaEventElapsedTime(&ms, ev[2 + 2 * it], ev[3 + 2 * it]));
-      wsum += ms;
+      for (int g = 0; g < G; ++g) {
+        PK_CUDA(cudaEventElapsedTime(&ms, gev(it, g), gev(it, g + 1)));
+        j->group_ms[g] += ms;
+        wsum += ms;
+      }
     }
     if (walk_ms) *walk_ms = wsum;
     for (auto& e : ev) cudaEventDestroy(e);
@@ -1273,6 +1382,31 @@ extern "C" int pk_job_info(pk_job* j, int64_t* info) {
     info[6] = j->smem;
     info[7] = j->kind == 0 ? 3 : static_cast<int64_t>(j->groups.size());
     return 0;
+  });
+}
+
+extern "C" int pk_job_groups(pk_job* j, int64_t* desc, double* ms, int64_t* prime_idx,
+                             int max_groups) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(j != nullptr, kErrArg, "null job");
+    if (j->kind != 1) return 0;
+    const int G = static_cast<int>(j->groups.size());
+    PK_CUDA(cudaSetDevice(j->c->dev));
+    for (int g = 0; g < std::min(G, max_groups); ++g) {
+      const ModpGroup& D = j->gdesc[g];
+      const ModpLaunch& L = j->groups[g];
+      if (desc) {
+        cudaFuncAttributes fa{};
+        PK_CUDA(cudaFuncGetAttributes(&fa, L.fn));
+        const int kind = D.wide ? 4 : D.pf ? (D.wf ? 3 : 2) : (D.lazy ? 1 : 0);
+        const int64_t v[6] = {kind, D.P, fa.numRegs, L.occ, L.grid, L.smem};
+        std::copy(v, v + 6, desc + 6 * g);
+      }
+      if (ms) ms[g] = g < static_cast<int>(j->group_ms.size()) ? j->group_ms[g] : 0.0;
+      if (prime_idx)
+        for (int q = 0; q < 4; ++q) prime_idx[4 * g + q] = q < D.P ? D.idx[q] : -1;
+    }
+    return G;
   });
 }
 

@@ -31,6 +31,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 #include "pk_common.cuh"
@@ -76,8 +77,9 @@ struct WalkArgs {
   // load and no register-file read for half of all steps.
   // (F_p kernels keep column 0 in shared memory: with parameter operands the
   // lazy walk measured 8-10 % slower, profiles/r1_modp_rates_c0.json.)
-  double col0[2 * 48];
+  alignas(16) double col0[2 * 48];  // read as double2 by the complex walker
 };
+static_assert(offsetof(WalkArgs, col0) % 16 == 0, "WalkArgs::col0 must be 16-byte aligned");
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
