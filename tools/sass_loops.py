@@ -1,7 +1,7 @@
 """SASS of the walk kernels' hot loops: listings + per-update pipe counts (no GPU needed).
 
-    python tools/sass_loops.py [--listings]   -> profiles/r2_sass_loops.json
-                                                 (+ profiles/r2_sass_<tag>.txt with --listings)
+    python tools/sass_loops.py [--listings TAG ...]  -> profiles/r2_sass_loops.json
+                                                       + profiles/r2_sass_<tag>.txt listings
 
 For each kernel it extracts the main loop (the largest backward-branch region of
 the SASS from the built object), counts opcodes, and converts them to per-unit
@@ -56,6 +56,9 @@ KERNELS = {
     "wide_36": ("_ZN2pk18walk_modp64_kernelILi36ELi1EEEvNS_8WalkArgsE", "inst_wide_p1_29.o",
                 36, 1, "IMAD.WIDE.U32", None, "walk_modp64_kernel<36, 1 prime> (Montgomery-64)"),
 }
+
+# the four hot loops of the bench (committed SASS listings)
+LISTED = ["f64c32", "red3_35", "hybw_36", "wide_36", "hyb_36"]
 
 FP64 = ("DFMA", "DMUL", "DADD")
 HALF = ("IMAD.WIDE", "IMAD.HI")
@@ -160,14 +163,12 @@ def analyse(tag, spec, listings):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--listings", action="store_true")
-    ap.add_argument("--only", nargs="*")
+    ap.add_argument("--listings", nargs="*", default=LISTED,
+                    help="tags whose full loop listing goes to profiles/r2_sass_<tag>.txt")
     args = ap.parse_args()
     out = {}
     for tag, spec in KERNELS.items():
-        if args.only and tag not in args.only:
-            continue
-        out[tag] = analyse(tag, spec, args.listings)
+        out[tag] = analyse(tag, spec, tag in args.listings)
         r = out[tag]
         print(f"{tag:10s} loop {r['loop_instructions']:5d} instr, {r['steps_per_iteration']:g} steps;"
               " per unit: " + ", ".join(f"{k} {v:.2f}" for k, v in r["smsp_cycles_per_unit"].items())
