@@ -18,6 +18,9 @@ from pathlib import Path
 import numpy as np
 
 _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpermkit_gpu.so"
+# experiment variants (tools/build_variant.py) only; the product library is _LIB_PATH
+if os.environ.get("PERMKIT_GPU_LIB"):
+    _LIB_PATH = Path(os.environ["PERMKIT_GPU_LIB"]).resolve()
 
 _u64 = ctypes.c_uint64
 _i64 = ctypes.c_int64

@@ -51,8 +51,8 @@ const char* last_error_cstr() { return g_last_error.c_str(); }
 struct Tables {
   const void* f64[2][2][kMaxN + 1] = {};          // [cplx][column 0 in param][N]
   const void* modp[2][kMaxP + 1][kMaxN + 1] = {};  // [lazy][P][N]
-  const void* hybrid[2][3][kMaxN + 1] = {};         // [wide fp][PI][N], one fp64 prime
-  const void* wide[kMaxPWide + 1][kMaxN + 1] = {};  // [P][N], Montgomery-64
+  const void* hybrid[2][kMaxN + 1] = {};            // [wide fp][N]: 1 lazy + 1 fp64 prime
+  const void* wide[2][kMaxPWide + 1][kMaxN + 1] = {};  // [lazy][P][N], Montgomery-64
 };
 
 static const Tables& tables() {
@@ -74,13 +74,13 @@ static const Tables& tables() {
     PK_FOR_EACH_RANGE(PK_REG)
 #undef PK_REG
 #define PK_REGH(lo, hi)                         \
-  register_hybrid_pi1_w0_##lo(t.hybrid[0][1]);  \
-  register_hybrid_pi2_w0_##lo(t.hybrid[0][2]);  \
-  register_hybrid_pi1_w1_##lo(t.hybrid[1][1]);  \
-  register_hybrid_pi2_w1_##lo(t.hybrid[1][2]);
+  register_hybrid_pi1_w0_##lo(t.hybrid[0]);    \
+  register_hybrid_pi1_w1_##lo(t.hybrid[1]);
     PK_FOR_EACH_HYBRID_RANGE(PK_REGH)
 #undef PK_REGH
-#define PK_REGW1(lo, hi) register_wide_p1_##lo(t.wide[1]);
+#define PK_REGW1(lo, hi)                 \
+  register_wide_l0_p1_##lo(t.wide[0][1]); \
+  register_wide_l1_p1_##lo(t.wide[1][1]);
     PK_FOR_EACH_RANGE(PK_REGW1)
 #undef PK_REGW1
     return t;
@@ -957,11 +957,14 @@ static ModpLaunch prepare_modp(DevCtx& c, const Plan& p, const ModpGroup& G, int
   ModpLaunch L{};
   if (G.wide) {
     PK_REQUIRE(P >= 1 && P <= kMaxPWide, kErrInternal, "bad wide prime group");
-    L.fn = tables().wide[P][p.n];
+    bool lazy64 = true;  // rows reduced every second step needs p < 2^60 (pk_walk64.cuh)
+    for (int q = 0; q < P; ++q) lazy64 = lazy64 && group_primes[q] < (1ull << 60);
+    L.fn = tables().wide[lazy64 ? 1 : 0][P][p.n];
     PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing wide F_p kernel instantiation");
     L.smem = (2 * p.m + 1) * P * col_stride(p.n, 8) * 8;
   } else if (pf) {
-    L.fn = tables().hybrid[G.wf ? 1 : 0][pi][p.n];
+    PK_REQUIRE(pi == 1 && pf == 1, kErrInternal, "hybrid groups are one lazy + one fp64 prime");
+    L.fn = tables().hybrid[G.wf ? 1 : 0][p.n];
     PK_REQUIRE(L.fn != nullptr, kErrInternal, "missing hybrid F_p kernel instantiation");
     const int int_words = ((2 * p.m + 1) * pi * col_stride(p.n, 4) + 1) & ~1;
     L.smem = int_words * 4 + (2 * p.m + 1) * pf * col_stride(p.n, 8) * 8;

@@ -23,17 +23,18 @@ constexpr int kMaxP = 4;   // primes per lane in the F_p kernel
 // hybrid (Montgomery + fp64 primes) kernels exist for N in [kHybridMinN, kMaxN]
 constexpr int kHybridMinN = 17;
 #define PK_FOR_EACH_HYBRID_RANGE(X) X(17, 28) X(29, 36) X(37, 42) X(43, 48)
+// (group_primes pairs one lazy Montgomery prime with one fp64 prime, PI = 1)
 #define PK_DECL_HYBRID(lo, hi)                         \
   void register_hybrid_pi1_w0_##lo(const void** tbl); \
-  void register_hybrid_pi2_w0_##lo(const void** tbl); \
-  void register_hybrid_pi1_w1_##lo(const void** tbl); \
-  void register_hybrid_pi2_w1_##lo(const void** tbl);
+  void register_hybrid_pi1_w1_##lo(const void** tbl);
 PK_FOR_EACH_HYBRID_RANGE(PK_DECL_HYBRID)
 #undef PK_DECL_HYBRID
 // wide (2^31 <= p < 2^62, Montgomery-64) kernels: one prime per lane (two per
 // lane measured 20-30 % slower per prime: register pressure, profiles/r1_modp_rates_wide2.json)
 constexpr int kMaxPWide = 1;
-#define PK_DECL_WIDE1(lo, hi) void register_wide_p1_##lo(const void** tbl);
+#define PK_DECL_WIDE1(lo, hi)                     \
+  void register_wide_l0_p1_##lo(const void** tbl); \
+  void register_wide_l1_p1_##lo(const void** tbl);
 PK_FOR_EACH_RANGE(PK_DECL_WIDE1)
 #undef PK_DECL_WIDE1
 PK_FOR_EACH_RANGE(PK_DECL_F64)

@@ -32,42 +32,73 @@ __device__ __forceinline__ uint64_t wmul32(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint32_t lo32(uint64_t v) { return static_cast<uint32_t>(v); }
 __device__ __forceinline__ uint32_t hi32(uint64_t v) { return static_cast<uint32_t>(v >> 32); }
 
-// x y = (w3 w2 w1 w0) in 32-bit words: four independent IMAD.WIDE.U32 partial
-// products (fmaheavy), the carries summed on the ALU pipe (add.cc / addc).
-// Folding carries into the 64-bit addend of the wide multiplies instead needs a
-// zero-extended register pair per addend (extra IMAD.MOV on the same pipe).
-__device__ __forceinline__ void mul128(uint64_t x, uint64_t y, uint32_t& w0, uint32_t& w1,
-                                       uint32_t& w2, uint32_t& w3) {
-  const uint64_t a = wmul32(lo32(x), lo32(y)), b = wmul32(lo32(x), hi32(y));
-  const uint64_t c = wmul32(hi32(x), lo32(y)), d = wmul32(hi32(x), hi32(y));
-  w0 = lo32(a);
-  asm("add.cc.u32 %0, %3, %4;\n\t"
-      "addc.cc.u32 %1, %5, %6;\n\t"
-      "addc.u32 %2, %7, 0;\n\t"
-      "add.cc.u32 %0, %0, %8;\n\t"
-      "addc.cc.u32 %1, %1, %9;\n\t"
-      "addc.u32 %2, %2, 0;"
-      : "=r"(w1), "=r"(w2), "=r"(w3)
-      : "r"(hi32(a)), "r"(lo32(b)), "r"(lo32(d)), "r"(hi32(b)), "r"(hi32(d)), "r"(lo32(c)),
-        "r"(hi32(c)));
-}
-
-// REDC(x y) for x, y < 2p: 9 IMAD.WIDE.U32 + 2 IMAD (~20 fmaheavy issue units)
-// and ~17 ALU carry adds (__umul64hi lowers to ~30 fmaheavy units).
+// REDC(x y) = x y 2^-64 mod p in (0, 2p), for x y < p 2^64 (x, y < 2^63).
+// Schoolbook over 32-bit limbs, arranged so that no addend needs a
+// zero-extended register pair (a 64-bit addend of IMAD.WIDE.U32 is a register
+// pair; zero-extending a 32-bit word into one costs two extra instructions):
+//   x y:  lo = x0 y0, mid = x0 y1 + x1 y0 (< 2^64 for x, y < 2^63: the second
+//         multiply takes the first as its addend), hi = x1 y1; the 64-bit
+//         halves follow with one add.cc / addc / addc carry chain;
+//   m  = lo64(x y) p' mod 2^64: one wide and two plain IMADs;
+//   hi64(m p): m1 p0 + (m0 p1 + hi(m0 p0)) is 65 bits: add.cc / addc / addc,
+//         then added to m1 p1 (its low 64 bits equal lo64(x y): no borrow).
+// 8 IMAD.WIDE.U32 + 1 IMAD.HI.U32 + 2 IMAD (40 fmaheavy SMSP cycles per warp)
+// and 8 carry-chain ALU instructions.
 __device__ __forceinline__ uint64_t redc64_lazy(uint64_t x, uint64_t y, uint64_t p,
                                                 uint64_t pinv) {
-  uint32_t l0, l1, h0, h1;
-  mul128(x, y, l0, l1, h0, h1);
-  // m = lo p' mod 2^64
-  const uint64_t u0 = wmul32(l0, lo32(pinv));
-  const uint32_t m1 = hi32(u0) + l0 * hi32(pinv) + l1 * lo32(pinv);
-  const uint64_t m = (static_cast<uint64_t>(m1) << 32) | lo32(u0);
-  // high word of m p (its low word equals lo by construction)
-  uint32_t s0, s1, t0, t1;
-  mul128(m, p, s0, s1, t0, t1);
-  const uint64_t hi = (static_cast<uint64_t>(h1) << 32) | h0;
-  const uint64_t t = (static_cast<uint64_t>(t1) << 32) | t0;
-  return hi - t + p;  // (0, 2p)
+  // one PTX block: left to the front end, the 64-bit adds of zero-extended
+  // words survived as VIADD-with-zero register copies (~5 per REDC)
+  uint64_t r;
+  asm("{\n\t"
+      ".reg .u32 x0, x1, y0, y1, p0, p1, q0, q1, l0, l1, d0, d1, m0, m1, t, e;\n\t"
+      ".reg .u32 a0, a1, b0, b1, w0, w1, s0, s1, c, h0, h1, r0, r1;\n\t"
+      ".reg .u64 lo, mid, hi, u0, a, b, w;\n\t"
+      "mov.b64 {x0, x1}, %1;\n\t"
+      "mov.b64 {y0, y1}, %2;\n\t"
+      "mov.b64 {p0, p1}, %3;\n\t"
+      "mov.b64 {q0, q1}, %4;\n\t"
+      // x y = lo + mid 2^32 + hi 2^64
+      "mul.wide.u32 lo, x0, y0;\n\t"
+      "mul.wide.u32 mid, x0, y1;\n\t"
+      "mad.wide.u32 mid, x1, y0, mid;\n\t"
+      "mul.wide.u32 hi, x1, y1;\n\t"
+      "mov.b64 {l0, t}, lo;\n\t"
+      "mov.b64 {s0, s1}, mid;\n\t"
+      "mov.b64 {w0, w1}, hi;\n\t"
+      "add.cc.u32 l1, t, s0;\n\t"
+      "addc.cc.u32 d0, w0, s1;\n\t"
+      "addc.u32 d1, w1, 0;\n\t"
+      // m = (l1 l0) p' mod 2^64
+      "mul.wide.u32 u0, l0, q0;\n\t"
+      "mov.b64 {m0, t}, u0;\n\t"
+      "mad.lo.u32 t, l0, q1, t;\n\t"
+      "mad.lo.u32 m1, l1, q0, t;\n\t"
+      // high 64 bits of m p = m1 p1 + (m1 p0 + m0 p1 + hi(m0 p0)) >> 32
+      "mul.wide.u32 a, m1, p0;\n\t"
+      "mul.wide.u32 b, m0, p1;\n\t"
+      "mul.hi.u32 e, m0, p0;\n\t"
+      "mul.wide.u32 w, m1, p1;\n\t"
+      "mov.b64 {a0, a1}, a;\n\t"
+      "mov.b64 {b0, b1}, b;\n\t"
+      "mov.b64 {w0, w1}, w;\n\t"
+      "add.cc.u32 s0, a0, b0;\n\t"
+      "addc.cc.u32 s1, a1, b1;\n\t"
+      "addc.u32 c, 0, 0;\n\t"
+      "add.cc.u32 s0, s0, e;\n\t"
+      "addc.cc.u32 s1, s1, 0;\n\t"
+      "addc.u32 c, c, 0;\n\t"
+      "add.cc.u32 h0, w0, s1;\n\t"
+      "addc.u32 h1, w1, c;\n\t"
+      // d - h + p in (0, 2p): lo(m p) = lo(x y), so no borrow from below
+      "sub.cc.u32 r0, d0, h0;\n\t"
+      "subc.u32 r1, d1, h1;\n\t"
+      "add.cc.u32 r0, r0, p0;\n\t"
+      "addc.u32 r1, r1, p1;\n\t"
+      "mov.b64 %0, {r0, r1};\n\t"
+      "}"
+      : "=l"(r)
+      : "l"(x), "l"(y), "l"(p), "l"(pinv));
+  return r;
 }
 
 __device__ __forceinline__ uint64_t min_u64(uint64_t a, uint64_t b) { return a < b ? a : b; }
@@ -120,7 +151,14 @@ __device__ void stage_modp64(uint64_t* sm, const uint64_t* a, const uint64_t* pr
   }
 }
 
-template <int N, int P>
+// LAZY (p < 2^60): rows are reduced only on every second step.  Invariant:
+// rows < 2p after a reduction; a flip adds < p + 1 (plus copy v < p, minus
+// copy p - v <= p), so the tree sees rows < 3p (odd steps) or < 4p (even
+// steps, reduced after their tree by one conditional subtraction of 2p), and
+// 16 p^2 < p 2^64 keeps every REDC output in (0, 2p).  A flip is then a plain
+// 64-bit add (2 ALU) plus half a reduction (6 ALU / 2), against 8 ALU for the
+// reduced form min(v, v - p).
+template <int N, int P, bool LAZY>
 struct Modp64Walker {
   static constexpr int NS = col_stride(N, 8);
   static constexpr int CS = P * NS;
@@ -227,12 +265,27 @@ struct Modp64Walker {
 #pragma unroll
           for (int j = 0; j < NS; j += 2) {
             const ulonglong2 c = *reinterpret_cast<const ulonglong2*>(col + q * NS + j);
-            upd(r[q][j], c.x, p(q));
-            if (j + 1 < N) upd(r[q][j + 1], c.y, p(q));
+            if constexpr (LAZY) {
+              r[q][j] += c.x;
+              if (j + 1 < N) r[q][j + 1] += c.y;
+            } else {
+              upd(r[q][j], c.x, p(q));
+              if (j + 1 < N) upd(r[q][j + 1], c.y, p(q));
+            }
           }
         }
       }
       tree(y);
+      if constexpr (LAZY) {
+        if (!(s & 1)) {  // warp-uniform: rows < 4p -> < 2p
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            const uint64_t p2 = 2 * p(q);
+#pragma unroll
+            for (int j = 0; j < N; ++j) r[q][j] = r[q][j] >= p2 ? r[q][j] - p2 : r[q][j];
+          }
+        }
+      }
       if (s & 1) {
         add_pair(ye, y);
       } else {
@@ -245,10 +298,10 @@ struct Modp64Walker {
 
 // One wide prime group per launch; modp_out holds a (lo, hi) 128-bit counter
 // per prime of the fold2^-64-scaled residues.
-template <int N, int P>
+template <int N, int P, bool LAZY>
 __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * P * 2))
     walk_modp64_kernel(const __grid_constant__ WalkArgs args) {
-  using W_ = Modp64Walker<N, P>;
+  using W_ = Modp64Walker<N, P, LAZY>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* slot = reinterpret_cast<uint64_t*>(smem_raw);
   const int warp = threadIdx.x >> 5;

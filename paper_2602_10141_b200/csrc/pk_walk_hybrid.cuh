@@ -100,7 +100,42 @@ struct FpPart {
   // near (N / kC + log2 kC) links.
   static constexpr int kC = N >= 16 ? 4 : (N >= 2 ? 2 : 1);
 
+  // Wide primes: a depth-first binary tree over the unreduced row sums, like
+  // the Montgomery tree (depth log2 N instead of N / kC + log2 kC links).  The
+  // two-product modmul takes leaf x leaf products (|h| <= n^2 p^2, the bound
+  // fp64w_prime_ok is stated for), so no leaf needs a reduce first.
+#ifndef PK_HYB_TREE
+#define PK_HYB_TREE 1
+#endif
+  static constexpr bool kTree = WF && PK_HYB_TREE;
+
   __device__ __forceinline__ void product(double* y) const {
+    if constexpr (kTree) {
+      constexpr int LOG = 7;
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        double st[LOG];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          double v = x[q][j];
+          int l = 0;
+#pragma unroll
+          for (; l < LOG && ((j >> l) & 1); ++l) v = modmul(st[l], v, q);
+          st[l] = v;
+        }
+        double acc = 0.0;
+        bool have = false;
+#pragma unroll
+        for (int l = 0; l < LOG; ++l) {
+          if ((N >> l) & 1) {
+            acc = have ? modmul(st[l], acc, q) : st[l];
+            have = true;
+          }
+        }
+        y[q] = acc;
+      }
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
       double ch[kC];
