@@ -291,7 +291,20 @@ def group_roofline(g, n, units, sms, mhz, sass):
     return out
 
 
-def crt_section(args, nat, modular, sms, mhz, rank, world, pkdist):
+def mix_ceiling(mix, name, achieved, sms, mhz):
+    """The walk against the in-run ceiling of its own instruction mix
+    (csrc/pk_mix.cu: the production step + pair loop without the Gray
+    bookkeeping and segment restarts), scaled to the walk's SM clock."""
+    m = mix.get(name)
+    if not m:
+        return None
+    ceil = m["units_per_clk_sm"] * sms * mhz * 1e6
+    return {"mix": name, "ceiling": ceil / 1e9, "unit": "G units/s", "achieved": achieved / 1e9,
+            "frac": achieved / ceil,
+            "basis": "units per SM clock of the mix kernel (clock64 spans) x SMs x walk SM clock"}
+
+
+def crt_section(args, nat, modular, sms, mhz, rank, world, pkdist, mix=None):
     """secondary.crt: exact perm(S_n) on three bases (see the module docstring)."""
     n = args.crt_n
     m = n - 1  # Glynn, the default expansion of schur_* (modular.py)
@@ -334,6 +347,10 @@ def crt_section(args, nat, modular, sms, mhz, rank, world, pkdist):
         for g in groups:
             units = g["P"] * n * float(length)
             gr = group_roofline(g, n, units, sms, mhz, sass)
+            if g["kind"].startswith("hybrid") and mix:
+                gr["mix_ceiling"] = mix_ceiling(
+                    mix, "hybrid_wide_36" if g["kind"] == "hybrid_wide" else "hybrid_36",
+                    units / (g["ms"] / 1e3), sms, mhz)
             gr["primes"] = [primes[i] for i in g["prime_idx"]]
             rec["groups"].append(gr)
             ideal_t += g["ms"] * gr["frac"]
@@ -435,6 +452,7 @@ def main():
     a = headline_matrix(n)
     start, length = pkdist.shard_range(n, rank, world)
     peaks = nat.measure_peaks(local)
+    mix = nat.measure_mix_ceilings(local)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     job = nat.Job.f64(a, "ryser", start, length, device=0)
     info = job.info()
@@ -520,6 +538,7 @@ def main():
                      # issue; DMUL/DADD issue slots carry 1 flop, so this fraction is lower
                      "fp64_tflops_peak": 2 * fp64_peak / 1e12,
                      "flop_frac": 8 * achieved / (2 * fp64_peak)},
+        "mix_ceiling": mix_ceiling(mix, "complex_32", achieved, sms, mhz) if n == 32 else None,
         "kernel": {**info, "walk_ms_per_step": walk_ms_max / args.steps},
         "peaks": {k: {"ops_per_s": v["ops_per_s"], "per_clk_sm": v["ops_per_clk_sm"]}
                   for k, v in peaks.items()},
@@ -536,7 +555,7 @@ def main():
                                          f"{dt:.2f} s wall"}
     if not args.no_secondary:
         sec = {}
-        sec["crt"] = crt_section(args, nat, modular, sms, mhz, rank, world, pkdist)
+        sec["crt"] = crt_section(args, nat, modular, sms, mhz, rank, world, pkdist, mix)
         if rank == 0 and world == 1:
             sec.update(secondary_c2(nat))
         out["secondary"] = sec

@@ -94,6 +94,26 @@ int pk_ryser_f64_blocks(const double* a, int n, int is_complex, int algo,
                         double* out);
 
 /*
+ * A caller's block plan of ONE matrix in one call (engine._run_plan for
+ * perm_blocked, reference engine.py:213-245, which calls kernels.ryser_partial
+ * per block on a thread pool).  out[4*i ..] = {s_re, s_im, c_re, c_im} and
+ * abs_sums[i] (optional) of block i, bit-identical to pk_ryser_f64 on
+ * (starts[i], lens[i]); the caller folds the pairs in block order as the
+ * reference does.  Blocks are split over ndev devices; on each, the aligned
+ * interiors run in as few walk launches as possible, one segmented reduce
+ * serves every block, and every ragged piece runs in one exact launch.
+ */
+int pk_ryser_f64_plan(const double* a, int n, int is_complex, int algo, const uint64_t* starts,
+                      const uint64_t* lens, int nblocks, int ndev, double* out,
+                      double* abs_sums);
+
+/* The reference's ordered combine of a plan's block pairs (engine.py:240-245:
+ * KahanAccumulator add(s); add(c) per block, Neumaier per component).
+ * pairs[4*i ..] as pk_ryser_f64_plan's out; out[4] = {sum_re, sum_im, comp_re,
+ * comp_im}; the value is sum + comp. */
+int pk_kahan_fold(const double* pairs, int nblocks, int is_complex, double out[4]);
+
+/*
  * Full-range permanents of B matrices (contiguous B x n x n), e.g. the
  * ensemble sampler (ensembles.py:142-158) and the geodesic sweep
  * (geodesics.py:153-179).  out[4*b ..] as in pk_ryser_f64 for matrix b;
@@ -165,6 +185,16 @@ void pk_job_destroy(pk_job* job);
  */
 int pk_measure_peaks(int device, double* out, int max_out);
 const char* pk_peak_names(void);
+
+/*
+ * Instruction-mix ceilings (csrc/pk_mix.cu): the production walker structs'
+ * step + pair loop with no Gray bookkeeping and no segment restarts, at the
+ * walk's occupancy.  out[3*i..] = {units/s, units per SM clock, mean SM MHz}
+ * (units: row updates, or prime-row updates) for the mixes named by
+ * pk_mix_names().  Returns the count.
+ */
+int pk_measure_mix_ceilings(int device, double* out, int max_out);
+const char* pk_mix_names(void);
 
 /* Dependent-chain latencies in SM cycles for the ops named by
  * pk_latency_names() (one warp, one chain).  Returns the count. */

@@ -63,6 +63,7 @@ def _bind(lib):
         "pk_max_n": (_int, []),
         "pk_ryser_f64": (_int, [_vp, _int, _int, _int, _u64, _u64, _int, P(_dbl), P(_dbl)]),
         "pk_ryser_f64_blocks": (_int, [_vp, _int, _int, _int, _vp, _vp, _int, _int, _vp]),
+        "pk_ryser_f64_plan": (_int, [_vp, _int, _int, _int, _vp, _vp, _int, _int, _vp, _vp]),
         "pk_ryser_f64_batch": (_int, [_vp, _int, _int, _int, _int, _int, _vp, _vp]),
         "pk_ryser_modp": (_int, [_vp, _vp, _int, _int, _int, _u64, _u64, _int, _vp]),
         "pk_job_f64_create": (_int, [_int, _vp, _int, _int, _int, _u64, _u64, P(_vp)]),
@@ -75,6 +76,9 @@ def _bind(lib):
         "pk_peak_names": (ctypes.c_char_p, []),
         "pk_measure_latencies": (_int, [_int, _vp, _int]),
         "pk_latency_names": (ctypes.c_char_p, []),
+        "pk_kahan_fold": (_int, [_vp, _int, _int, _vp]),
+        "pk_measure_mix_ceilings": (_int, [_int, _vp, _int]),
+        "pk_mix_names": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -88,9 +92,10 @@ def exported_symbols():
     return [
         "pk_last_error", "pk_device_count", "pk_set_device_base", "pk_set_logical_devices",
         "pk_version", "pk_max_n", "pk_ryser_f64",
-        "pk_ryser_f64_blocks", "pk_ryser_f64_batch", "pk_ryser_modp", "pk_job_f64_create",
+        "pk_ryser_f64_blocks", "pk_ryser_f64_plan", "pk_ryser_f64_batch", "pk_ryser_modp", "pk_job_f64_create",
         "pk_job_modp_create", "pk_job_run", "pk_job_info", "pk_job_groups", "pk_job_destroy",
         "pk_measure_peaks", "pk_peak_names", "pk_measure_latencies", "pk_latency_names",
+        "pk_kahan_fold", "pk_measure_mix_ceilings", "pk_mix_names",
     ]
 
 
@@ -183,6 +188,22 @@ def ryser_f64_blocks(a: np.ndarray, algo: str, starts, lens, device: int = 0) ->
     return out
 
 
+def ryser_f64_plan(a: np.ndarray, algo: str, starts, lens, devices: int = 1,
+                   want_abs: bool = False):
+    """Per-block (sum, comp) pairs of one matrix over a block plan in one call;
+    returns ([nblocks, 4] float64 {s_re, s_im, c_re, c_im}, [nblocks] abs or None)."""
+    cplx = np.iscomplexobj(a)
+    a = np.ascontiguousarray(a, dtype=np.complex128 if cplx else np.float64)
+    s = np.ascontiguousarray(starts, dtype=np.uint64)
+    ln = np.ascontiguousarray(lens, dtype=np.uint64)
+    out = np.zeros((len(s), 4), dtype=np.float64)
+    ab = np.zeros(len(s), dtype=np.float64) if want_abs else None
+    _check(lib().pk_ryser_f64_plan(_ptr(a), a.shape[0], int(cplx), PK_ALGO[algo], _ptr(s), _ptr(ln),
+                                   len(s), int(devices), _ptr(out),
+                                   _ptr(ab) if want_abs else None))
+    return out, ab
+
+
 def ryser_f64_batch(mats: np.ndarray, algo: str, devices: int = 1, want_abs: bool = False):
     """Full-range partials of B matrices; returns ([B,4] float64, [B] abs or None)."""
     cplx = np.iscomplexobj(mats)
@@ -215,6 +236,28 @@ def measure_peaks(device: int = 0) -> dict:
     names = lib().pk_peak_names().decode().split(",")
     return {names[i]: {"ops_per_s": float(buf[3 * i]), "ops_per_clk_sm": float(buf[3 * i + 1]),
                        "sm_mhz": float(buf[3 * i + 2])} for i in range(k)}
+
+
+def measure_mix_ceilings(device: int = 0) -> dict:
+    """In-run ceilings of the walks' instruction mixes (csrc/pk_mix.cu)."""
+    buf = np.zeros(48, dtype=np.float64)
+    k = lib().pk_measure_mix_ceilings(int(device), _ptr(buf), 48)
+    if k < 0:
+        _check(k)
+    names = lib().pk_mix_names().decode().split(",")
+    return {names[i]: {"units_per_s": float(buf[3 * i]), "units_per_clk_sm": float(buf[3 * i + 1]),
+                       "sm_mhz": float(buf[3 * i + 2])} for i in range(k)}
+
+
+def kahan_fold(pairs: np.ndarray, is_complex: bool):
+    """engine._run_plan's ordered combine (reference engine.py:240-245) in C:
+    returns (sum, comp) of the per-block [s_re, s_im, c_re, c_im] rows."""
+    pairs = np.ascontiguousarray(pairs, dtype=np.float64)
+    out = np.zeros(4, dtype=np.float64)
+    _check(lib().pk_kahan_fold(_ptr(pairs), pairs.shape[0], int(is_complex), _ptr(out)))
+    if is_complex:
+        return complex(out[0], out[1]), complex(out[2], out[3])
+    return float(out[0]), float(out[2])
 
 
 def measure_latencies(device: int = 0) -> dict:

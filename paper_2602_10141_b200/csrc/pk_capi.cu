@@ -213,6 +213,11 @@ static int occupancy(DevCtx& c, const void* fn, int threads, int smem) {
 // ---------------------------------------------------------------------------
 // plans
 
+// Ragged ends of unaligned ranges are walked by the exact kernel (one thread per
+// piece, a serial chain: ~0.5-1 us per step), in aligned pieces of <= 2^6
+// indices so that many short pieces run in parallel.
+constexpr int kPieceBits = 6;
+
 struct Plan {
   int n = 0, m = 0, k = 0;   // k = 0: no aligned tiles (tiny m), everything ragged
   uint64_t tiles_total = 0;  // aligned tiles per matrix over the whole range
@@ -238,7 +243,7 @@ static Plan make_plan(int n, int algo) {
   p.k = std::max(kmin, m - kTileBits - 17);
   p.tiles_total = 1ull << (m - p.k - kTileBits);
   p.group = std::max<uint64_t>(1, p.tiles_total / kMaxGroups);
-  p.piece_bits = std::min(p.k, 10);
+  p.piece_bits = std::min(p.k, kPieceBits);
   return p;
 }
 
@@ -256,7 +261,7 @@ static Plan make_plan_per_matrix(int n, int algo) {
   p.k = std::max(kmin, p.m - kTileBits - 10);
   p.tiles_total = 1ull << (p.m - p.k - kTileBits);
   p.group = std::max<uint64_t>(1, p.tiles_total / kMaxGroups);
-  p.piece_bits = std::min(p.k, 10);
+  p.piece_bits = std::min(p.k, kPieceBits);
   return p;
 }
 static bool batch_per_matrix(int m, bool cplx) {
@@ -698,6 +703,180 @@ extern "C" int pk_ryser_f64(const double* a, int n, int is_complex, int algo, ui
     out[2] = v.re.c;
     out[3] = v.im.c;
     if (abs_sum) *abs_sum = v.ab;
+    return 0;
+  });
+}
+
+namespace pk {
+
+// A caller's block plan on one device: blocks [b0, b1).  Every block gets the
+// root and pieces a single-range call on it would (same plan, groups, tree and
+// piece cuts), so node[b] is bit-identical to f64_range on the block.  The
+// aligned interiors are walked in as few launches as possible (runs of blocks
+// whose interiors are adjacent up to a few tiles share one launch), then one
+// segmented fold and one segmented tree reduce every block, and one exact
+// launch walks every block's ragged pieces.
+static void f64_plan_device(DevCtx& c, const double* a, int n, bool cplx, int algo, const Plan& p,
+                            const std::vector<Range>& rs, int b0, int b1, bool want_abs,
+                            std::vector<Node>& node) {
+  const size_t abytes = static_cast<size_t>(n) * n * (cplx ? 16 : 8);
+  auto* d_a = static_cast<double*>(c.a.get(abytes));
+  PK_CUDA(cudaMemcpyAsync(d_a, a, abytes, cudaMemcpyHostToDevice, c.stream));
+  // runs of interiors (blocks in order; a gap of <= 4 tiles is walked, not split)
+  struct Run {
+    uint64_t lo, hi, pidx;
+  };
+  std::vector<Run> runs;
+  std::vector<uint64_t> pbase(b1 - b0, 0);
+  uint64_t ptotal = 0;
+  for (int b = b0; b < b1; ++b) {
+    const Range& r = rs[b];
+    if (r.t1 <= r.t0) continue;
+    if (!runs.empty() && r.t0 >= runs.back().lo && r.t0 <= runs.back().hi + 4) {
+      Run& u = runs.back();
+      if (r.t1 > u.hi) {
+        ptotal += r.t1 - u.hi;
+        u.hi = r.t1;
+      }
+    } else {
+      runs.push_back(Run{r.t0, r.t1, ptotal});
+      ptotal += r.t1 - r.t0;
+    }
+    const Run& u = runs.back();
+    pbase[b - b0] = u.pidx + (r.t0 - u.lo);
+  }
+  std::vector<FoldTask> ft;
+  std::vector<TreeTask> tt;
+  std::vector<int> tree_block;
+  for (int b = b0; b < b1; ++b) {
+    const Range& r = rs[b];
+    if (r.t1 <= r.t0) continue;
+    const uint64_t g0 = r.t0 / p.group, g1 = (r.t1 - 1) / p.group + 1;
+    tt.push_back(TreeTask{g0, static_cast<int>(ft.size()), static_cast<int>(g1 - g0)});
+    tree_block.push_back(b);
+    for (uint64_t g = g0; g < g1; ++g) {
+      const uint64_t lo = std::max(g * p.group, r.t0), hi = std::min((g + 1) * p.group, r.t1);
+      ft.push_back(FoldTask{lo, hi, pbase[b - b0] + (lo - r.t0)});
+    }
+  }
+  if (!runs.empty()) {
+    auto* d_part = static_cast<double*>(c.partials.get(ptotal * kPartialStride * 8));
+    for (const Run& u : runs) {
+      F64Launch L = prepare_f64(c, p, cplx, algo, 1, d_a, u.lo, u.hi - u.lo, want_abs,
+                                d_part + u.pidx * kPartialStride, a);
+      launch_walk(c, L.fn, L.grid, L.smem, L.args);
+    }
+    // task tables and group nodes share the `groups` scratch: tasks first
+    const size_t ft_bytes = (ft.size() * sizeof(FoldTask) + 255) & ~size_t(255);
+    const size_t tt_bytes = (tt.size() * sizeof(TreeTask) + 255) & ~size_t(255);
+    auto* scratch = static_cast<uint8_t*>(
+        c.groups.get(ft_bytes + tt_bytes + ft.size() * kPartialStride * 8));
+    auto* d_ft = reinterpret_cast<FoldTask*>(scratch);
+    auto* d_tt = reinterpret_cast<TreeTask*>(scratch + ft_bytes);
+    auto* d_grp = reinterpret_cast<double*>(scratch + ft_bytes + tt_bytes);
+    auto* d_out = static_cast<double*>(c.out.get(tt.size() * kPartialStride * 8));
+    PK_CUDA(cudaMemcpyAsync(d_ft, ft.data(), ft.size() * sizeof(FoldTask), cudaMemcpyHostToDevice,
+                            c.stream));
+    PK_CUDA(cudaMemcpyAsync(d_tt, tt.data(), tt.size() * sizeof(TreeTask), cudaMemcpyHostToDevice,
+                            c.stream));
+    const int nft = static_cast<int>(ft.size());
+    fold_tasks_kernel<<<(nft + kFoldThreads - 1) / kFoldThreads, kFoldThreads, 0, c.stream>>>(
+        d_part, d_ft, nft, d_grp);
+    PK_CUDA(cudaGetLastError());
+    tree_tasks_kernel<<<static_cast<int>(tt.size()), kTreeThreads, 0, c.stream>>>(d_grp, d_tt, d_out);
+    PK_CUDA(cudaGetLastError());
+    std::vector<double> h(tt.size() * kPartialStride);
+    PK_CUDA(cudaMemcpyAsync(h.data(), d_out, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+    PK_CUDA(cudaStreamSynchronize(c.stream));
+    for (size_t i = 0; i < tt.size(); ++i) node[tree_block[i]] = node_from5(&h[i * kPartialStride]);
+  }
+  // every block's ragged pieces in one exact launch, then the index-order fold
+  std::vector<std::pair<uint64_t, uint64_t>> pcs;
+  for (int b = b0; b < b1; ++b) {
+    pcs.insert(pcs.end(), rs[b].head.begin(), rs[b].head.end());
+    pcs.insert(pcs.end(), rs[b].tail.begin(), rs[b].tail.end());
+  }
+  const std::vector<Node> pv = run_f64_pieces(c, d_a, n, cplx, algo, pcs, want_abs);
+  size_t k = 0;
+  for (int b = b0; b < b1; ++b) {
+    const Range& r = rs[b];
+    std::vector<Node> seq(pv.begin() + k, pv.begin() + k + r.head.size());
+    k += r.head.size();
+    if (r.t1 > r.t0) seq.push_back(node[b]);
+    seq.insert(seq.end(), pv.begin() + k, pv.begin() + k + r.tail.size());
+    k += r.tail.size();
+    Node acc{};
+    if (!seq.empty()) {
+      acc = seq[0];
+      for (size_t i = 1; i < seq.size(); ++i) acc = node_combine_h(acc, seq[i]);
+    }
+    node[b] = acc;
+  }
+}
+
+}  // namespace pk
+
+extern "C" int pk_ryser_f64_plan(const double* a, int n, int is_complex, int algo,
+                                 const uint64_t* starts, const uint64_t* lens, int nblocks,
+                                 int ndev, double* out, double* abs_sums) {
+  return pk_guard([&]() -> int {
+    check_f64_args(a, n, algo);
+    PK_REQUIRE(nblocks >= 0, kErrArg, "negative block count");
+    if (nblocks == 0) return 0;
+    PK_REQUIRE(starts && lens && out, kErrArg, "null block arrays");
+    const bool cplx = is_complex != 0;
+    const Plan p = make_plan(n, algo);
+    std::vector<Range> rs(nblocks);
+    for (int b = 0; b < nblocks; ++b) {
+      check_range(p.m, starts[b], lens[b]);
+      rs[b] = make_range(p, starts[b], lens[b]);
+    }
+    ndev = std::min(clamp_ndev(ndev), nblocks);
+    std::vector<Node> node(nblocks);
+    for_devices(ndev, [&](int d) {
+      const int b0 = static_cast<int>(static_cast<int64_t>(nblocks) * d / ndev);
+      const int b1 = static_cast<int>(static_cast<int64_t>(nblocks) * (d + 1) / ndev);
+      if (b1 <= b0) return;
+      DevCtx& c = ctx(d);
+      std::lock_guard<std::mutex> g(c.mu);
+      PK_CUDA(cudaSetDevice(c.dev));
+      f64_plan_device(c, a, n, cplx, algo, p, rs, b0, b1, abs_sums != nullptr, node);
+    });
+    for (int b = 0; b < nblocks; ++b) {
+      out[4 * b + 0] = node[b].re.s;
+      out[4 * b + 1] = node[b].im.s;
+      out[4 * b + 2] = node[b].re.c;
+      out[4 * b + 3] = node[b].im.c;
+      if (abs_sums) abs_sums[b] = node[b].ab;
+    }
+    return 0;
+  });
+}
+
+// The reference's ordered combine of block partials (engine.py:240-245:
+// KahanAccumulator add(s); add(c) per block, Neumaier per component,
+// engine.py:33-73), so that a plan of thousands of blocks costs no Python loop.
+extern "C" int pk_kahan_fold(const double* pairs, int nblocks, int is_complex, double out[4]) {
+  return pk_guard([&]() -> int {
+    PK_REQUIRE(nblocks >= 0 && (nblocks == 0 || pairs) && out, kErrArg, "bad fold arguments");
+    double s[2] = {0.0, 0.0}, c[2] = {0.0, 0.0};
+    auto add = [&](int z, double v) {
+      const double t = s[z] + v;
+      const bool big_s = std::fabs(s[z]) >= std::fabs(v);
+      c[z] += big_s ? ((s[z] - t) + v) : ((v - t) + s[z]);
+      s[z] = t;
+    };
+    for (int b = 0; b < nblocks; ++b) {
+      const double* q = pairs + 4 * b;  // s_re, s_im, c_re, c_im
+      add(0, q[0]);
+      if (is_complex) add(1, q[1]);
+      add(0, q[2]);
+      if (is_complex) add(1, q[3]);
+    }
+    out[0] = s[0];
+    out[1] = s[1];
+    out[2] = c[0];
+    out[3] = c[1];
     return 0;
   });
 }

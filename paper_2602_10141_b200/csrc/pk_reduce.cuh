@@ -67,13 +67,11 @@ __global__ void __launch_bounds__(kFoldThreads) fold_groups_kernel(
 // Stage 2: binary tree over the groups on GLOBAL indices (level L node j covers
 // groups [j 2^L, (j+1) 2^L)); missing children pass their sibling through.  The
 // first kRegLevels levels are combined in registers, the rest in shared memory.
-__global__ void __launch_bounds__(kTreeThreads) tree_groups_kernel(const double* __restrict__ groups,
-                                                                    uint64_t g0, int ng,
-                                                                    double* __restrict__ out) {
+// G: the ng group nodes of global groups [g0, g0 + ng); one CTA.
+__device__ __forceinline__ void tree_groups_body(const double* __restrict__ G, uint64_t g0, int ng,
+                                                 double* __restrict__ out) {
   constexpr int kLeaves = 1 << kRegLevels;
   __shared__ Node5 buf[2][kMaxGroups / kLeaves + 2];
-  const int b = blockIdx.x;
-  const double* G = groups + static_cast<uint64_t>(b) * ng * kPartialStride;
   const uint64_t g1 = g0 + ng;  // exclusive
   uint64_t lo_prev = g0 >> kRegLevels, hi_prev = (g1 - 1) >> kRegLevels;
   const int cnt0 = static_cast<int>(hi_prev - lo_prev + 1);
@@ -122,7 +120,53 @@ __global__ void __launch_bounds__(kTreeThreads) tree_groups_kernel(const double*
     lo_prev = lo;
     hi_prev = hi;
   }
-  if (threadIdx.x == 0) store_node(out + static_cast<uint64_t>(b) * kPartialStride, buf[cur][0]);
+  if (threadIdx.x == 0) store_node(out, buf[cur][0]);
+}
+
+// One CTA per matrix b: groups [b][ng] of global groups [g0, g0 + ng).
+__global__ void __launch_bounds__(kTreeThreads) tree_groups_kernel(const double* __restrict__ groups,
+                                                                    uint64_t g0, int ng,
+                                                                    double* __restrict__ out) {
+  const int b = blockIdx.x;
+  tree_groups_body(groups + static_cast<uint64_t>(b) * ng * kPartialStride, g0, ng,
+                   out + static_cast<uint64_t>(b) * kPartialStride);
+}
+
+// ---------------------------------------------------------------------------
+// Segmented forms for a caller's block plan (pk_ryser_f64_plan): one launch
+// reduces every block's own tile range with exactly the groups and tree a
+// single-range call on that block would use, so each block's root is
+// bit-identical to pk_ryser_f64 on the block.
+//
+// Fold task i: global tiles [lo_i, hi_i), whose partials sit at consecutive
+// indices from pidx_i -> group node i (a left fold, as fold_groups_kernel).
+struct FoldTask {
+  uint64_t lo, hi, pidx;
+};
+__global__ void __launch_bounds__(kFoldThreads) fold_tasks_kernel(
+    const double* __restrict__ partials, const FoldTask* __restrict__ tasks, int ntasks,
+    double* __restrict__ groups) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntasks) return;
+  const FoldTask t = tasks[i];
+  const double* P = partials + t.pidx * kPartialStride;
+  Node5 acc = load_node(P);
+  for (uint64_t x = 1; x < t.hi - t.lo; ++x) acc = node_combine(acc, load_node(P + x * kPartialStride));
+  store_node(groups + static_cast<uint64_t>(i) * kPartialStride, acc);
+}
+
+// Tree of block b: its groups are nodes [first_b, first_b + ng_b) of `groups`,
+// global group indices [g0_b, g0_b + ng_b).
+struct TreeTask {
+  uint64_t g0;
+  int first, ng;
+};
+__global__ void __launch_bounds__(kTreeThreads) tree_tasks_kernel(const double* __restrict__ groups,
+                                                                   const TreeTask* __restrict__ tasks,
+                                                                   double* __restrict__ out) {
+  const TreeTask t = tasks[blockIdx.x];
+  tree_groups_body(groups + static_cast<uint64_t>(t.first) * kPartialStride, t.g0, t.ng,
+                   out + static_cast<uint64_t>(blockIdx.x) * kPartialStride);
 }
 
 }  // namespace pk

@@ -39,6 +39,15 @@
 #ifndef PK_MINCTA_T
 #define PK_MINCTA_T 64
 #endif
+// Column 0 in the kernel parameter: read element by element (0, default) or as
+// 16-byte double2 vectors from an alignas(16) field (1).  The element-wise form
+// keeps round 1's parameter layout, which measured 1.5 % faster on the complex
+// n = 32 walk (57.45 vs 58.4 ms, profiles/r2_col0_layout.txt) -- a scheduling
+// effect of the layout, since both read column 0 as LDCU.128 -- and needs no
+// cast of the parameter to double2 (no misaligned vector access).
+#ifndef PK_COL0_ALIGN
+#define PK_COL0_ALIGN 0
+#endif
 namespace pk {
 
 constexpr int kWalkThreads = 128;  // 4 warps per CTA
@@ -77,9 +86,15 @@ struct WalkArgs {
   // load and no register-file read for half of all steps.
   // (F_p kernels keep column 0 in shared memory: with parameter operands the
   // lazy walk measured 8-10 % slower, profiles/r1_modp_rates_c0.json.)
+#if PK_COL0_ALIGN
   alignas(16) double col0[2 * 48];  // read as double2 by the complex walker
+#else
+  double col0[2 * 48];  // read element by element (F64Walker::step_c0)
+#endif
 };
+#if PK_COL0_ALIGN
 static_assert(offsetof(WalkArgs, col0) % 16 == 0, "WalkArgs::col0 must be 16-byte aligned");
+#endif
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
@@ -225,6 +240,7 @@ struct F64Walker {
   double s_re, c_re, s_im, c_im, abs_acc;
   bool want_abs;
   const T* c0;  // C0P: column 0 in the __grid_constant__ parameter
+  const double* c0d;  // the same, as doubles (PK_COL0_ALIGN = 0)
   // shared minus copies of the walk columns (DADD flips): single-matrix kernels
   // only; in the batched kernels (a slot per warp) they measured -1 to -15 %
   static constexpr bool kMinus = C0P;
@@ -266,6 +282,17 @@ struct F64Walker {
   // flip one column with direction sg and return the new term's product
   __device__ __forceinline__ T step(const T* __restrict__ col, double sg) {
     update(col, sg);
+    return tree();
+  }
+  // column 0 from the kernel parameter, read element by element
+  __device__ __forceinline__ T step_c0(const double* __restrict__ c, double sg) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if constexpr (CPLX)
+        fma_upd(r[j], sg, make_double2(c[2 * j], c[2 * j + 1]));
+      else
+        fma_upd(r[j], sg, c[j]);
+    }
     return tree();
   }
 
@@ -358,7 +385,8 @@ struct F64Walker {
       // shared-memory column 0: (e >> 31) is always 0; it keeps the column
       // from being hoisted out of the loop into registers (spilling the state)
       const bool mo = StepPlan::minus_odd(e + 1, k, lane_minus);
-      const T po = C0P      ? step(c0, mo ? -1.0 : 1.0)
+      const T po = C0P      ? (PK_COL0_ALIGN ? step(c0, mo ? -1.0 : 1.0)
+                                             : step_c0(c0d, mo ? -1.0 : 1.0))
                    : kMinus ? step((mo ? W + m * NS : W) + (e >> 31) * NS, 1.0)
                             : step(W + (e >> 31) * NS, mo ? -1.0 : 1.0);
       add_pair(pe, po);
@@ -417,6 +445,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
   W_ w;
   w.want_abs = args.want_abs != 0;
   w.c0 = C0P ? reinterpret_cast<const T*>(args.col0) : nullptr;
+  w.c0d = C0P ? args.col0 : nullptr;
   // Ryser's global sign (-1)^n: the term sign at a segment start (its Gray
   // code has even popcount).  Negation is exact and commutes with the TwoSum
   // tree, so it is applied per lane.

@@ -266,16 +266,13 @@ def _run_plan(a, domain, plan, devices):
     _validate_plan(plan, n)
     algorithm = plan.algorithm
     if domain is COMPLEX or domain is REAL:
-        acc = KahanAccumulator(complex_valued=domain is COMPLEX)
-        for blk in plan.blocks:
-            if blk.length == 0:
-                s = c = 0j if domain is COMPLEX else 0.0
-            else:
-                s, c, _ = _native.ryser_f64(a, algorithm, blk.start, blk.length,
-                                            _devices(devices))
-            acc.add(s)
-            acc.add(c)
-        return _float_result(acc.value, domain, n, algorithm)
+        # one C-ABI call for the whole plan (pk_ryser_f64_plan): every block's
+        # pair is the one a single-range call on it returns; then the
+        # reference's ordered KahanAccumulator combine (pk_kahan_fold)
+        parts, _ = _native.ryser_f64_plan(a, algorithm, [b.start for b in plan.blocks],
+                                          [b.length for b in plan.blocks], _devices(devices))
+        s, c = _native.kahan_fold(parts, domain is COMPLEX)
+        return _float_result(s + c, domain, n, algorithm)
     return _run_full(a, domain, n, algorithm, devices)
 
 

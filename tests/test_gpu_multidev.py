@@ -175,3 +175,46 @@ def test_tiny_batch_single_launch(gpu):
     for i in (0, 250, 499):
         s, c, _ = gpu.ryser_f64(mats[i], "ryser", 0, 32)
         assert bits_equal(s + c, got[i])
+
+
+@pytest.mark.parametrize("kind,n,algo,nblocks", [("haar-u", 24, "ryser", 512),
+                                                 ("haar-o", 22, "glynn", 96),
+                                                 ("ginibre-c", 13, "ryser", 300)])
+def test_plan_call_matches_single_range_calls(logical8, kind, n, algo, nblocks):
+    """pk_ryser_f64_plan (perm_blocked's one call per plan, reference
+    engine.py:213-245): every block's pair equals pk_ryser_f64 on that block, bit
+    for bit, on 1 and 8 devices; uneven (make_block_plan) and irregular plans."""
+    from paper_2602_10141_b200.gray import make_block_plan
+    gpu = logical8
+    a = ensembles.sample_matrix(kind, n, 4, 0)
+    m = n if algo == "ryser" else n - 1
+    plan = make_block_plan(n, algo, nblocks)
+    starts = [b.start for b in plan.blocks]
+    lens = [b.length for b in plan.blocks]
+    rng = np.random.default_rng(n)
+    cuts = np.sort(rng.choice(np.arange(1, 1 << m), size=40, replace=False))
+    bounds = [0, *cuts.tolist(), 1 << m]
+    irr_s, irr_l = bounds[:-1], [b - a_ for a_, b in zip(bounds[:-1], bounds[1:])]
+    for st, ln in ((starts, lens), (irr_s, irr_l)):
+        one, ab1 = gpu.ryser_f64_plan(a, algo, st, ln, devices=1, want_abs=True)
+        eight, ab8 = gpu.ryser_f64_plan(a, algo, st, ln, devices=8, want_abs=True)
+        assert np.array_equal(one.view(np.uint64), eight.view(np.uint64))
+        assert np.array_equal(ab1, ab8)
+        for i in list(range(0, len(st), max(1, len(st) // 17))) + [len(st) - 1]:
+            s, c, ab = gpu.ryser_f64(a, algo, st[i], ln[i], want_abs=True)
+            s, c = complex(s), complex(c)
+            row = one[i]
+            assert bits_equal(s, complex(row[0], row[1])) and bits_equal(c, complex(row[2], row[3])), i
+            assert ab == ab1[i]
+
+
+def test_perm_blocked_plan_vs_oracle(gpu):
+    """perm_blocked through the plan call against the oracle's plan combine."""
+    from paper_2602_10141_b200 import engine
+    from paper_2602_10141_b200.gray import make_block_plan
+    a = ensembles.sample_matrix("haar-u", 18, 9, 0)
+    plan = make_block_plan(18, "ryser", 37)
+    got = engine.perm_blocked(a, plan)
+    ref = oracle.permanent(a, "ryser", blocks=37)
+    s, c, ab = gpu.ryser_f64(a, "ryser", 0, 1 << 18, want_abs=True)
+    assert abs(got - ref) <= 8 * 18 * 2.0 ** -53 * ab + 4 * 2.0 ** -53 * abs(ref)

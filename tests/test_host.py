@@ -303,3 +303,24 @@ def test_device_base_validation():
     with pytest.raises(_native.GpuError):
         _native.set_device_base(_native.device_count() + 3)
     _native.set_device_base(0)
+
+
+def test_kahan_fold_matches_kahan_accumulator():
+    """pk_kahan_fold (C, in the library; no device needed) is engine._run_plan's
+    ordered combine: bit-identical to KahanAccumulator add(s); add(c) per block
+    (reference engine.py:33-73, 240-245)."""
+    import numpy as np
+
+    from paper_2602_10141_b200 import _native
+    from paper_2602_10141_b200.engine import KahanAccumulator
+    rng = np.random.default_rng(5)
+    for cplx in (True, False):
+        rows = rng.standard_normal((300, 4)) * np.exp(rng.uniform(-30, 30, (300, 1)))
+        if not cplx:
+            rows[:, 1] = rows[:, 3] = 0.0
+        acc = KahanAccumulator(complex_valued=cplx)
+        for r in rows:
+            acc.add(complex(r[0], r[1]) if cplx else r[0])
+            acc.add(complex(r[2], r[3]) if cplx else r[2])
+        s, c = _native.kahan_fold(rows, cplx)
+        assert s == acc.sum and c == acc.compensation

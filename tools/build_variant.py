@@ -4,9 +4,11 @@
 
 Recompiles only the named instantiation objects (stems of the Makefile's
 build/inst_*.o, e.g. hyb_pi1_w1_29 = walk_hybrid_kernel<29..36, 1, 1, wide>) with
-the extra -D flags into paper_2602_10141_b200/csrc/build_var/NAME/, links them
-with every other object of build/ into paper_2602_10141_b200/_lib_var/NAME.so,
-and prints the path.  Select it at run time with PERMKIT_GPU_LIB=<path>
+the extra -D flags into paper_2602_10141_b200/csrc/build_var/NAME/ and links them
+with pk_capi.o, pk_peaks.o and weak no-op stand-ins for every other kernel
+table's registration function into paper_2602_10141_b200/_lib_var/NAME.so (a
+few MB instead of the full library's ~160 MB: gpurun snapshots are capped), and
+prints the path.  Only the named kernels exist in a variant library.  Select it at run time with PERMKIT_GPU_LIB=<path>
 (paper_2602_10141_b200/_native.py); the product library is untouched.
 """
 import os
@@ -49,6 +51,8 @@ def defines(stem):
 
 def main():
     name, flags, stems = sys.argv[1], sys.argv[2].split(), sys.argv[3:]
+    capi_flag = "--capi" in flags
+    flags = [f for f in flags if f != "--capi"]
     out_dir = os.path.join(CSRC, "build_var", name)
     os.makedirs(out_dir, exist_ok=True)
 
@@ -67,8 +71,23 @@ def main():
     with ThreadPoolExecutor(8) as pool:
         new = list(pool.map(compile_one, stems))
     base = os.path.join(CSRC, "build")
-    objs = [os.path.join(base, f) for f in sorted(os.listdir(base)) if f.endswith(".o")
-            and f[len("inst_"):-2] not in stems]
+    stems_all = sorted(f[len("inst_"):-2] for f in os.listdir(base)
+                       if f.startswith("inst_") and f.endswith(".o"))
+    stub = os.path.join(out_dir, "stubs.cu")
+    with open(stub, "w") as f:
+        f.write("namespace pk {\n")
+        for st in stems_all:
+            if st not in stems:
+                f.write(f"__attribute__((weak)) void register_{st.replace('hyb_', 'hybrid_')}"
+                        "(const void**) {}\n")
+        f.write("}\n")
+    subprocess.run(["nvcc", *NVFLAGS, "-c", stub, "-o", stub[:-3] + ".o"], check=True)
+    capi = os.path.join(base, "pk_capi.o")
+    if capi_flag:  # the flags change a host/device shared layout: recompile the ABI too
+        capi = os.path.join(out_dir, "pk_capi.o")
+        subprocess.run(["nvcc", *NVFLAGS, *flags, "-c", os.path.join(CSRC, "pk_capi.cu"), "-o", capi],
+                       check=True)
+    objs = [capi, os.path.join(base, "pk_peaks.o"), stub[:-3] + ".o"]
     lib_dir = os.path.join(ROOT, "paper_2602_10141_b200", "_lib_var")
     os.makedirs(lib_dir, exist_ok=True)
     lib = os.path.join(lib_dir, f"{name}.so")
