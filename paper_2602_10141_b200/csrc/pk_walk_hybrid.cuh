@@ -100,12 +100,14 @@ struct FpPart {
   // near (N / kC + log2 kC) links.
   static constexpr int kC = N >= 16 ? 4 : (N >= 2 ? 2 : 1);
 
-  // Wide primes: a depth-first binary tree over the unreduced row sums, like
-  // the Montgomery tree (depth log2 N instead of N / kC + log2 kC links).  The
-  // two-product modmul takes leaf x leaf products (|h| <= n^2 p^2, the bound
-  // fp64w_prime_ok is stated for), so no leaf needs a reduce first.
+  // PK_HYB_TREE = 1 (wide primes): a depth-first binary tree over the
+  // unreduced row sums, like the Montgomery tree (depth log2 N instead of
+  // N / kC + log2 kC links); the two-product modmul takes leaf x leaf products
+  // (|h| <= n^2 p^2, the bound fp64w_prime_ok is stated for).  It measured the
+  // same as the chains (profiles/r2_hybrid_variants.txt): the walk already runs
+  // at its mix ceiling (profiles/r2_hybrid_mix.txt), so the chains stay.
 #ifndef PK_HYB_TREE
-#define PK_HYB_TREE 1
+#define PK_HYB_TREE 0
 #endif
   static constexpr bool kTree = WF && PK_HYB_TREE;
 
