@@ -49,7 +49,7 @@ const char* last_error_cstr() { return g_last_error.c_str(); }
 // kernel tables
 
 struct Tables {
-  const void* f64[2][2][kMaxN + 1] = {};          // [cplx][column 0 in param][N]
+  const void* f64[2][2][kMaxNReal + 1] = {};      // [cplx][column 0 in param][N]; N > 48: real
   const void* modp[2][kMaxP + 1][kMaxN + 1] = {};  // [lazy][P][N]
   const void* hybrid[2][kMaxN + 1] = {};            // [wide fp][N]: 1 lazy + 1 fp64 prime
   const void* wide[2][kMaxPWide + 1][kMaxN + 1] = {};  // [lazy][P][N], Montgomery-64
@@ -73,6 +73,8 @@ static const Tables& tables() {
   register_modp_l1_p4_##lo(t.modp[1][4]);
     PK_FOR_EACH_RANGE(PK_REG)
 #undef PK_REG
+    register_f64_c0_p0_49(t.f64[0][0]);
+    register_f64_c0_p1_49(t.f64[0][1]);
 #define PK_REGH(lo, hi)                         \
   register_hybrid_pi1_w0_##lo(t.hybrid[0]);    \
   register_hybrid_pi1_w1_##lo(t.hybrid[1]);
@@ -241,6 +243,10 @@ static Plan make_plan(int n, int algo) {
   // tiles of 2^kTileBits segments of 2^k indices; ~2^17 tiles per matrix
   const int kmin = std::min(m - kTileBits, 8);
   p.k = std::max(kmin, m - kTileBits - 17);
+  // test / measurement hook ($PK_PLAN_K, read per call): force the segment
+  // bits, e.g. so that a tile of an n > 48 walk (2^(m - 17) indices per lane
+  // by default) is short enough for an oracle comparison or a rate sample
+  if (const int kf = env_int("PK_PLAN_K", 0); kf > 0) p.k = std::clamp(kf, 1, m - kTileBits);
   p.tiles_total = 1ull << (m - p.k - kTileBits);
   p.group = std::max<uint64_t>(1, p.tiles_total / kMaxGroups);
   p.piece_bits = std::min(p.k, kPieceBits);
@@ -344,10 +350,12 @@ struct F64Launch {
 static F64Launch prepare_f64(DevCtx& c, const Plan& p, bool cplx, int algo, int B,
                              const double* d_a, uint64_t t0, uint64_t nt, bool want_abs,
                              double* d_partials, const double* h_a = nullptr) {
-  PK_REQUIRE(p.n >= 1 && p.n <= kMaxN, kErrLimit,
+  const int nmax = cplx ? kMaxN : kMaxNReal;
+  PK_REQUIRE(p.n >= 1 && p.n <= nmax, kErrLimit,
              "dimension " + std::to_string(p.n) + " exceeds the GPU kernel range n <= " +
-                 std::to_string(kMaxN));
+                 std::to_string(nmax) + (cplx ? " (complex)" : " (real)"));
   static_assert(sizeof(WalkArgs::col0) / sizeof(double) >= 2 * kMaxN, "col0 too small");
+  static_assert(sizeof(WalkArgs::col0) / sizeof(double) >= kMaxNReal, "col0 too small");
   F64Launch L{};
   const bool c0p = B == 1 && h_a != nullptr && p.m >= 1;
   L.fn = tables().f64[cplx ? 1 : 0][c0p ? 1 : 0][p.n];

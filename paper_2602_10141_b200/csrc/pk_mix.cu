@@ -42,41 +42,36 @@ __device__ __forceinline__ void mix_span(long long t0, MixOut* spans) {
   }
 }
 
-// complex fp64: the C0P walk's step pair -- even step from a shared-memory
-// column (plus / minus copy, DADD flips), odd step from column 0 in the kernel
-// parameter (fma(+-1) flips) -- and its compensated pair accumulation.
+// complex fp64: the FP64 work of the walk's step pair -- n fma(+-1) row flips
+// and the production product tree (F64Walker::tree) per step, the pair
+// difference and its Neumaier step (F64Walker::add_pair) -- with the column in
+// registers: the ceiling of the arithmetic mix itself, without the column
+// loads (round 1's tools/micro/fp64_mix.cu measured 88 % of the DFMA peak for
+// the same mix without the Neumaier step).
 template <int N>
 __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * 4))
     mix_complex_kernel(const __grid_constant__ WalkArgs args, int pairs, double* sink,
                        MixOut* spans) {
-  using W_ = F64Walker<N, true, true>;
+  using W_ = F64Walker<N, true, false>;
   using T = double2;
-  constexpr int NS = W_::NS;
-  __shared__ __align__(16) T col[2][kMixCols][NS];
-  for (int j = threadIdx.x; j < kMixCols * NS; j += blockDim.x) {
-    const T v = make_double2(1e-3 * (j + 1), -2e-3 * (j + 2));
-    col[0][0][j] = v;
-    col[1][0][j] = make_double2(-v.x, -v.y);
-  }
-  __syncthreads();
   W_ w;
   w.want_abs = false;
-  w.c0 = reinterpret_cast<const T*>(args.col0);
-  w.c0d = args.col0;
-  for (int j = 0; j < N; ++j) w.r[j] = make_double2(0.5 + 1e-3 * j + 1e-6 * threadIdx.x, 0.25);
+  T c[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    w.r[j] = make_double2(0.9 + 1e-3 * j + 1e-6 * threadIdx.x, 0.1);
+    c[j] = make_double2(1e-3 * j, 2e-3);
+  }
   w.s_re = w.c_re = w.s_im = w.c_im = w.abs_acc = 0.0;
   const long long t0 = clock64();
-#pragma unroll 1
   for (int e = 0; e < pairs; ++e) {
-    const int d = e & 1;  // add, then remove: the state stays bounded
-    // the column varies as the walk's even-step column ctz(e) does, so no
-    // column can be hoisted into registers
-    const int b = (__ffs(e >> 1) - 1) & (kMixCols - 1);
-    const T pe = w.step(col[d][b], 1.0);
-    // (e >> 30) is always 0: keeps column 0 from being hoisted into registers,
-    // as in F64Walker::walk_sub
-    const T po = PK_COL0_ALIGN ? w.step(w.c0 + (e >> 30) * NS, d ? -1.0 : 1.0)
-                               : w.step_c0(w.c0d + (e >> 30) * 2 * NS, d ? -1.0 : 1.0);
+    const double sg = (e & 1) ? -1.0 : 1.0;  // add, then remove: the state stays bounded
+#pragma unroll
+    for (int j = 0; j < N; ++j) fma_upd(w.r[j], sg, c[j]);
+    const T pe = w.tree();
+#pragma unroll
+    for (int j = 0; j < N; ++j) fma_upd(w.r[j], -sg, c[j]);
+    const T po = w.tree();
     w.add_pair(pe, po);
   }
   mix_span(t0, spans);

@@ -4,6 +4,9 @@
 namespace pk {
 
 constexpr int kMaxN = 48;  // largest state length with a register-resident kernel
+// real fp64 walks go further: 64 doubles of state fit the register file (the
+// paper's 54 x 54 real Glynn permanent)
+constexpr int kMaxNReal = 64;
 constexpr int kMaxP = 4;   // primes per lane in the F_p kernel
 
 // N ranges compiled per object; must match the Makefile's INST_RANGES.
@@ -38,6 +41,8 @@ constexpr int kMaxPWide = 1;
 PK_FOR_EACH_RANGE(PK_DECL_WIDE1)
 #undef PK_DECL_WIDE1
 PK_FOR_EACH_RANGE(PK_DECL_F64)
+void register_f64_c0_p0_49(const void** tbl);  // real, N = 49..64
+void register_f64_c0_p1_49(const void** tbl);
 PK_FOR_EACH_RANGE(PK_DECL_MODP)
 #undef PK_DECL_F64
 #undef PK_DECL_MODP

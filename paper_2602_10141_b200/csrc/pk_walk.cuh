@@ -48,6 +48,9 @@
 #ifndef PK_COL0_ALIGN
 #define PK_COL0_ALIGN 0
 #endif
+#ifndef PK_PAIR4
+#define PK_PAIR4 0
+#endif
 namespace pk {
 
 constexpr int kWalkThreads = 128;  // 4 warps per CTA
@@ -341,6 +344,21 @@ struct F64Walker {
     }
   }
 
+  __device__ __forceinline__ void add_quad(T pe, T po, T qe, T qo) {
+    const T d = sub2(pe, po);
+    const T f = sub2(qe, qo);
+    if constexpr (CPLX) {
+      neumaier(s_re, c_re, d.x + f.x);
+      neumaier(s_im, c_im, d.y + f.y);
+      if (want_abs)
+        abs_acc += ((fabs(pe.x) + fabs(pe.y)) + (fabs(po.x) + fabs(po.y))) +
+                   ((fabs(qe.x) + fabs(qe.y)) + (fabs(qo.x) + fabs(qo.y)));
+    } else {
+      neumaier(s_re, c_re, d + f);
+      if (want_abs) abs_acc += (fabs(pe) + fabs(po)) + (fabs(qe) + fabs(qo));
+    }
+  }
+
   static constexpr int kSubBits = 12;
   __device__ __forceinline__ void walk(const T* __restrict__ base, const T* __restrict__ W, int m,
                                        int k, uint64_t seg) {
@@ -375,22 +393,40 @@ struct F64Walker {
                           : step(W + (start >> 63) * NS, mo ? -1.0 : 1.0);
       add_pair(pe, po);
     }
-    for (uint32_t e = 2; e < L; e += 2) {
+    auto pair_at = [&](uint32_t e, T& pe, T& po) {
       const int b = __ffs(e) - 1;
       // with minus copies (Wm = W + m NS) the update is a DADD: +1.5 % against
       // fma(+-1, col, r) (profiles/r1_walk_experiments_c0.txt)
       const bool me = StepPlan::minus_even(e, k, lane_minus);
-      const T pe = kMinus ? step((me ? W + m * NS : W) + b * NS, 1.0)
-                          : step(W + b * NS, me ? -1.0 : 1.0);
+      pe = kMinus ? step((me ? W + m * NS : W) + b * NS, 1.0) : step(W + b * NS, me ? -1.0 : 1.0);
       // shared-memory column 0: (e >> 31) is always 0; it keeps the column
       // from being hoisted out of the loop into registers (spilling the state)
       const bool mo = StepPlan::minus_odd(e + 1, k, lane_minus);
-      const T po = C0P      ? (PK_COL0_ALIGN ? step(c0, mo ? -1.0 : 1.0)
-                                             : step_c0(c0d, mo ? -1.0 : 1.0))
-                   : kMinus ? step((mo ? W + m * NS : W) + (e >> 31) * NS, 1.0)
-                            : step(W + (e >> 31) * NS, mo ? -1.0 : 1.0);
+      po = C0P      ? (PK_COL0_ALIGN ? step(c0, mo ? -1.0 : 1.0) : step_c0(c0d, mo ? -1.0 : 1.0))
+           : kMinus ? step((mo ? W + m * NS : W) + (e >> 31) * NS, 1.0)
+                    : step(W + (e >> 31) * NS, mo ? -1.0 : 1.0);
+    };
+#if PK_PAIR4
+    // two step pairs per compensated add: d = (t0 - t1) + (t2 - t3), one
+    // Neumaier step per four terms (error <= 3 u (|t0| + ... + |t3|), inside
+    // the n u S gate); L = 2^k >= 4 here (k >= 2 whenever tiles exist)
+    for (uint32_t e = 2; e < L; e += 4) {
+      T pe, po, qe, qo;
+      pair_at(e, pe, po);
+      if (e + 2 < L) {
+        pair_at(e + 2, qe, qo);
+        add_quad(pe, po, qe, qo);
+      } else {
+        add_pair(pe, po);
+      }
+    }
+#else
+    for (uint32_t e = 2; e < L; e += 2) {
+      T pe, po;
+      pair_at(e, pe, po);
       add_pair(pe, po);
     }
+#endif
   }
 };
 

@@ -40,6 +40,10 @@ from .gray import GLYNN, RYSER, BlockPlan, iteration_exponent
 
 NAIVE_MAX_N = 11
 GRAY_MAX_N = 48   # reference: 40 (engine.py:25); lifted to the GPU kernels' range
+# real fp64 walks: 64 rows of state fit the register file (the paper's 54 x 54
+# real Glynn permanent); Ryser's 2^64 range of n = 64 does not
+# fit a uint64 length, so Ryser stops at 63
+REAL_MAX_N = {RYSER: 63, GLYNN: 64}
 ABS_MAX_N = 25
 
 
@@ -123,7 +127,12 @@ def _normalize(a, domain):
     return out, domain, n
 
 
-def _check_gray_dims(n):
+def _check_gray_dims(n, domain=None, algorithm=None):
+    if domain is REAL and algorithm in REAL_MAX_N and n > GRAY_MAX_N:
+        if n > REAL_MAX_N[algorithm]:
+            raise LimitError(f"dimension {n} exceeds the n <= {REAL_MAX_N[algorithm]} range "
+                             f"of real {algorithm}")
+        return
     if n > GRAY_MAX_N:
         raise LimitError(f"dimension {n} exceeds the n <= {GRAY_MAX_N} range")
 
@@ -283,7 +292,7 @@ def perm_blocked(a, plan: BlockPlan, worker_count: int = 1,
                  domain: ScalarDomain | None = None, devices: int | None = None):
     """Permanent via a block plan; bit-identical for any worker_count."""
     a, domain, n = _normalize(a, domain)
-    _check_gray_dims(n)
+    _check_gray_dims(n, domain, plan.algorithm)
     if isinstance(domain, PrimeField) and plan.algorithm == GLYNN and domain.p == 2:
         raise ValueError("division by two unavailable in GF(2)")
     return _run_plan(a, domain, plan, devices)
@@ -293,7 +302,7 @@ def perm_ryser(a, domain: ScalarDomain | None = None, threads: int = 1,
                devices: int | None = None):
     """Ryser's inclusion-exclusion permanent in Gray-code order (GPU)."""
     a, domain, n = _normalize(a, domain)
-    _check_gray_dims(n)
+    _check_gray_dims(n, domain, RYSER)
     return _run_full(a, domain, n, RYSER, devices)
 
 
@@ -301,7 +310,7 @@ def perm_glynn(a, domain: ScalarDomain | None = None, threads: int = 1,
                devices: int | None = None):
     """Glynn's 2^(n-1)-term expansion in Gray-code order (GPU)."""
     a, domain, n = _normalize(a, domain)
-    _check_gray_dims(n)
+    _check_gray_dims(n, domain, GLYNN)
     if isinstance(domain, PrimeField) and domain.p == 2:
         raise ValueError("division by two unavailable in GF(2)")
     return _run_full(a, domain, n, GLYNN, devices)
@@ -346,7 +355,7 @@ def perm_batch(mats, method: str = "ryser", devices: int | None = None,
     if method == "naive":
         vals = np.array([perm_naive(m) for m in mats])
         return (vals, None) if want_abs else vals
-    _check_gray_dims(n)
+    _check_gray_dims(n, COMPLEX if np.iscomplexobj(mats) else REAL, method)
     if method not in (RYSER, GLYNN):
         raise ValueError(f"unknown method {method!r}")
     cplx = np.iscomplexobj(mats)

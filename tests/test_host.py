@@ -121,7 +121,12 @@ def test_input_validation_matches_reference_messages():
     with pytest.raises(ValueError, match="empty matrix"):
         engine.perm_ryser(np.zeros((0, 0)))
     with pytest.raises(engine.LimitError, match="exceeds the n <= 48 range"):
-        engine.perm_ryser(np.eye(49))
+        engine.perm_ryser(np.eye(49, dtype=complex))
+    # real fp64 walks go to n = 63 (Ryser) / 64 (Glynn), beyond the reference's 40
+    with pytest.raises(engine.LimitError, match="exceeds the n <= 63 range of real ryser"):
+        engine.perm_ryser(np.eye(64))
+    with pytest.raises(engine.LimitError, match="exceeds the n <= 64 range of real glynn"):
+        engine.perm_glynn(np.eye(65))
     with pytest.raises(engine.LimitError, match="exceeds the n <= 25 range"):
         engine.perm_abs_entrywise(np.eye(26))
     with pytest.raises(engine.LimitError, match="oracle dimension exceeded"):
