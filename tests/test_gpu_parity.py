@@ -314,13 +314,40 @@ def test_schur_a003112_gpu_basis(gpu, n):
         assert v31 == A003112[n]
 
 
-def test_schur_36_two_bases_agree(gpu):
-    v1, b1, _ = modular.schur_permanent_fast(36)
-    assert v1 == 0  # even n
-    v35, _, w35 = modular.schur_permanent_fast(35)
-    v35b, _, _ = modular.schur_permanent_exact(35, max_bits=31)
-    assert v35 == v35b
-    assert abs(v35) <= 35 ** 17.5
+def _ref_large():
+    """perm(S_n) for n >= 35 from the REFERENCE's own CPU path (tools/pin_schur_ref.py:
+    modular.schur_residue / perm_blocked over GF(p), reference modular.py:160-206)."""
+    return {r["n"]: r for r in load_golden("schur_ref_large.json")["rows"] if r.get("value")}
+
+
+@pytest.mark.parametrize("n", sorted(_ref_large()))
+def test_schur_large_n_matches_reference_cpu_path(gpu, n):
+    """The north_star's target beyond the CPU's reach at n >= 35: perm(S_n) on the GPU
+    basis (Glynn), on the reference's 31-bit basis (Ryser, its expansion) and on its
+    default 59-bit basis (Montgomery-64 walk) all equal the value the reference's
+    own CPU pipeline produced, and every 31-bit residue equals the reference's."""
+    row = _ref_large()[n]
+    want = int(row["value"])
+    v, _, _ = modular.schur_permanent_fast(n)
+    assert v == want
+    v31, b31, w31 = modular.schur_permanent_exact(n, max_bits=31, method="ryser")
+    assert v31 == want
+    assert list(b31.primes) == row["primes"]
+    assert [w.residue for w in w31] == row["residues"]
+    assert [w.root for w in w31] == row["roots"]
+    v59, _, _ = modular.schur_permanent_exact(n)  # the reference's default basis
+    assert v59 == want
+
+
+def test_schur_odd_n_cross_expansion(gpu):
+    """Odd n (an even n gives 0, which proves nothing): Ryser and Glynn walks of the
+    same prime give the same residue at n = 37 on the GPU basis."""
+    b = modular.gpu_prime_basis(37)
+    g = modular.schur_residues(37, b.primes, method="glynn")
+    r = modular.schur_residues(37, b.primes, method="ryser")
+    assert [w.residue for w in g] == [w.residue for w in r]
+    v = modular.crt_reconstruct(g, b)
+    assert v != 0 and abs(v) <= 37 ** 18.5
 
 
 # --------------------------------------------------------------------------- engine KATs

@@ -75,3 +75,25 @@ def test_oracle_schur_values():
             pw = [pow(root, k, p) for k in range(n)]
             a = [[pw[(j * k) % n] for k in range(n)] for j in range(n)]
             assert oracle.permanent_modp(a, p, blocks=8) == res
+
+
+def test_reference_pinned_large_schur_values_consistent():
+    """The reference-produced perm(S_n), n >= 35 (tests/golden/schur_ref_large.json,
+    tools/pin_schur_ref.py): the CRT lift of the reference's residues is the stored
+    value, every residue is that value mod its prime, and each root is a primitive
+    n-th root of unity (reference modular.py:126-147)."""
+    from conftest import load_golden
+    from paper_2602_10141_b200 import modular
+    for row in load_golden("schur_ref_large.json")["rows"]:
+        if not row.get("value"):
+            continue
+        n, v = row["n"], int(row["value"])
+        basis = modular.find_primes(n, max_bits=31)
+        assert list(basis.primes) == row["primes"]
+        wit = [modular.ResidueWitness(prime=p, root=g, residue=r)
+               for p, g, r in zip(row["primes"], row["roots"], row["residues"])]
+        assert modular.crt_reconstruct(wit, basis) == v
+        for p, g, r in zip(row["primes"], row["roots"], row["residues"]):
+            assert v % p == r
+            assert g == modular.primitive_nth_root(p, n)
+        assert v % 2 == 1 and abs(v) <= n ** (n / 2)
