@@ -26,7 +26,7 @@ def test_real_beyond_48_tiles_vs_oracle(gpu, monkeypatch, n, algo):
     a = np.abs(ensembles.sample_matrix("ginibre-r", n, 2602, 1)) / np.sqrt(n)
     m = n if algo == "ryser" else n - 1
     span = 8 << 15  # eight tiles
-    st = int(np.random.default_rng(n).integers(0, 1 << 40)) * span
+    st = int(np.random.default_rng(n).integers(0, (1 << m) // span - 1)) * span
     parts = 64
     rows = oracle.run_blocks(a, [st + i * (span // parts) for i in range(parts)],
                              [span // parts] * parts, algo)
