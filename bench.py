@@ -437,9 +437,17 @@ def main():
     from paper_2602_10141_b200 import dist as pkdist
     from paper_2602_10141_b200 import engine, modular
 
+    # test hook for the N > 1 code path on a one-GPU box: every rank on GPU 0,
+    # gloo instead of NCCL (NCCL refuses two ranks on one GPU).  The ranks'
+    # walks are independent, so sharing the GPU only serialises them.
+    if os.environ.get("PK_BENCH_SHARE_GPU") == "1":
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("PK_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
