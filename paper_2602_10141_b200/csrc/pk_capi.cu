@@ -389,6 +389,9 @@ static F64Launch prepare_f64(DevCtx& c, const Plan& p, bool cplx, int algo, int 
     for (int i = 0; i < n; ++i)
       for (int z = 0; z < w; ++z)
         a.col0[w * i + z] = algo == 0 ? h_a[w * (i * n) + z] : -2.0 * h_a[w * (n + i) + z];
+#if PK_PAIR4
+    std::copy(std::begin(a.col0), std::end(a.col0), std::begin(a.col0b));
+#endif
   }
   return L;
 }

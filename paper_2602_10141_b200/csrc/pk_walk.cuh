@@ -94,6 +94,9 @@ struct WalkArgs {
 #else
   double col0[2 * 48];  // read element by element (F64Walker::step_c0)
 #endif
+#if PK_PAIR4
+  double col0b[2 * 48];  // a second copy of col0 (experiment PK_PAIR4)
+#endif
 };
 #if PK_COL0_ALIGN
 static_assert(offsetof(WalkArgs, col0) % 16 == 0, "WalkArgs::col0 must be 16-byte aligned");
@@ -244,6 +247,7 @@ struct F64Walker {
   bool want_abs;
   const T* c0;  // C0P: column 0 in the __grid_constant__ parameter
   const double* c0d;  // the same, as doubles (PK_COL0_ALIGN = 0)
+  const double* c0d2;  // PK_PAIR4: the second copy (WalkArgs::col0b)
   // shared minus copies of the walk columns (DADD flips): single-matrix kernels
   // only; in the batched kernels (a slot per warp) they measured -1 to -15 %
   static constexpr bool kMinus = C0P;
@@ -414,7 +418,13 @@ struct F64Walker {
       T pe, po, qe, qo;
       pair_at(e, pe, po);
       if (e + 2 < L) {
+        // the second odd step reads the parameter's second copy of column 0
+        // (WalkArgs::col0b): distinct uniform loads, not one copy held in
+        // vector registers across the body
+        const double* keep = c0d;
+        if (C0P) c0d = c0d2;
         pair_at(e + 2, qe, qo);
+        c0d = keep;
         add_quad(pe, po, qe, qo);
       } else {
         add_pair(pe, po);
@@ -482,6 +492,11 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * (CPLX ? 4 : 2)))
   w.want_abs = args.want_abs != 0;
   w.c0 = C0P ? reinterpret_cast<const T*>(args.col0) : nullptr;
   w.c0d = C0P ? args.col0 : nullptr;
+#if PK_PAIR4
+  w.c0d2 = C0P ? args.col0b : nullptr;
+#else
+  w.c0d2 = w.c0d;
+#endif
   // Ryser's global sign (-1)^n: the term sign at a segment start (its Gray
   // code has even popcount).  Negation is exact and commutes with the TwoSum
   // tree, so it is applied per lane.
@@ -593,6 +608,22 @@ struct ModpWalker {
     else
       r = addmod_red(r, c, p);
   }
+  // The step's row update.  PK_ALU_ADD: a third, runtime-zero operand (a
+  // uniform kernel parameter) makes the add a 3-input IADD3, which only the ALU
+  // pipe executes; a 2-input add may be issued as IMAD.IADD on the fmaheavy
+  // pipe, the pipe the REDCs are bound by.
+#ifndef PK_ALU_ADD
+#define PK_ALU_ADD 0
+#endif
+  uint32_t zero = 0;
+  __device__ __forceinline__ void upd_step(uint32_t& r, uint32_t c, uint32_t p) const {
+    if constexpr (PK_ALU_ADD) {
+      const uint32_t v = r + c + zero;
+      r = LAZY ? v : min(v, v - p);
+    } else {
+      upd(r, c, p);
+    }
+  }
 
   // REDC product tree, evaluated depth-first like the fp64 tree (N - 1 REDCs,
   // scale 2^(-32 (N-1))).  Bounds: lazy rows are < 2^31 and every REDC output
@@ -645,10 +676,10 @@ struct ModpWalker {
 #pragma unroll
       for (int j = 0; j < NS; j += 4) {
         const uint4 c = *reinterpret_cast<const uint4*>(col + q * NS + j);
-        upd(r[q][j], c.x, p(q));
-        if (j + 1 < N) upd(r[q][j + 1], c.y, p(q));
-        if (j + 2 < N) upd(r[q][j + 2], c.z, p(q));
-        if (j + 3 < N) upd(r[q][j + 3], c.w, p(q));
+        upd_step(r[q][j], c.x, p(q));
+        if (j + 1 < N) upd_step(r[q][j + 1], c.y, p(q));
+        if (j + 2 < N) upd_step(r[q][j + 2], c.z, p(q));
+        if (j + 3 < N) upd_step(r[q][j + 3], c.w, p(q));
       }
     }
     tree(y);
@@ -713,6 +744,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * P))
   __syncthreads();
   W_ w;
   w.mc = &args.mc;
+  w.zero = static_cast<uint32_t>(args.per_warp_slot);  // always 0 for F_p launches
   unsigned long long tot[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) tot[q] = 0;

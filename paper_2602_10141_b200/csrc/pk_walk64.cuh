@@ -26,6 +26,11 @@
 
 namespace pk {
 
+#ifndef PK_WIDE_UNROLL
+#define PK_WIDE_UNROLL 1
+#endif
+constexpr int kWideUnroll = PK_WIDE_UNROLL;  // steps per loop body (experiment)
+
 __device__ __forceinline__ uint64_t wmul32(uint32_t a, uint32_t b) {
   return static_cast<uint64_t>(a) * b;  // IMAD.WIDE.U32
 }
@@ -164,6 +169,7 @@ struct Modp64Walker {
   static constexpr int CS = P * NS;
 
   uint64_t r[P][N];
+  uint64_t zero = 0;  // a runtime zero (PK_ALU_ADD)
   const ModConsts* mc;
   uint64_t acc_lo[P], acc_hi[P];  // exact 128-bit sum of the segment's terms
 
@@ -255,6 +261,7 @@ struct Modp64Walker {
     // instructions, and the two-step body of the 32-bit walk overflowed the
     // instruction cache here (ncu: 2.1 no_instruction stalls per issue).
     uint64_t y[P], ye[P];
+#pragma unroll kWideUnroll
     for (uint32_t s = 0; s < L; ++s) {
       if (s) {
         const int b = __ffs(s) - 1;
@@ -266,8 +273,10 @@ struct Modp64Walker {
           for (int j = 0; j < NS; j += 2) {
             const ulonglong2 c = *reinterpret_cast<const ulonglong2*>(col + q * NS + j);
             if constexpr (LAZY) {
-              r[q][j] += c.x;
-              if (j + 1 < N) r[q][j + 1] += c.y;
+              // PK_ALU_ADD: a runtime-zero third operand keeps the 64-bit add on
+              // the ALU pipe (3-input IADD3 / IADD3.X; see pk_walk.cuh upd_step)
+              r[q][j] += c.x + (PK_ALU_ADD ? zero : 0ull);
+              if (j + 1 < N) r[q][j + 1] += c.y + (PK_ALU_ADD ? zero : 0ull);
             } else {
               upd(r[q][j], c.x, p(q));
               if (j + 1 < N) upd(r[q][j + 1], c.y, p(q));
@@ -282,7 +291,8 @@ struct Modp64Walker {
           for (int q = 0; q < P; ++q) {
             const uint64_t p2 = 2 * p(q);
 #pragma unroll
-            for (int j = 0; j < N; ++j) r[q][j] = r[q][j] >= p2 ? r[q][j] - p2 : r[q][j];
+            for (int j = 0; j < N; ++j)
+              r[q][j] = r[q][j] >= p2 ? r[q][j] - p2 + (PK_ALU_ADD ? zero : 0ull) : r[q][j];
           }
         }
       }
@@ -313,6 +323,7 @@ __global__ void __launch_bounds__(kWalkThreads, min_ctas(N * P * 2))
   __syncthreads();
   W_ w;
   w.mc = &args.mc;
+  w.zero = static_cast<uint64_t>(args.per_warp_slot);  // always 0 for F_p launches
   uint64_t tot[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) tot[q] = 0;
