@@ -513,7 +513,7 @@ def main():
     achieved = args.steps * per_gpu_upd / (walk_ms_max / 1e3)
     traffic = None
     try:  # DRAM bytes per walk launch from the committed ncu capture (profiles/)
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             traffic = json.load(f).get(f"walk_f64_kernel<{n},true>")
     except OSError:
         pass
