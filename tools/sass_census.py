@@ -1,5 +1,8 @@
 """SASS opcode census of the walk kernels in the built library (no GPU needed).
 
+Round 2: superseded by tools/sass_loops.py (the Gray-step loop rather than the
+largest loop, per-unit pipe cycles, listings); kept for profiles/r1_sass_census.txt.
+
     python tools/sass_census.py > profiles/r1_sass_census.txt
 Proves the instruction classes the rooflines assume: DFMA/DMUL (FP64 pipe) for the
 fp64 walk, IMAD.WIDE.U32 / IMAD / IMAD.HI.U32 (REDC) and IADD3 (lazy row update)
@@ -17,8 +20,8 @@ KERNELS = [
     ("walk_f64_kernel<23, complex, batched>", r"_ZN2pk15walk_f64_kernelILi23ELb1ELb0EEEvNS_8WalkArgsE"),
     ("walk_modp_kernel<36, 3, reduced>", r"_ZN2pk16walk_modp_kernelILi36ELi3ELb0EEEvNS_8WalkArgsE"),
     ("walk_modp_kernel<36, 4, lazy>", r"_ZN2pk16walk_modp_kernelILi36ELi4ELb1EEEvNS_8WalkArgsE"),
-    ("walk_hybrid_kernel<36, 1, 1>", r"_ZN2pk18walk_hybrid_kernelILi36ELi1ELi1EEEvNS_8WalkArgsE"),
-    ("walk_modp64_kernel<32, 1>", r"_ZN2pk18walk_modp64_kernelILi32ELi1EEEvNS_8WalkArgsE"),
+    ("walk_hybrid_kernel<36, 1, 1, wide>", r"_ZN2pk18walk_hybrid_kernelILi36ELi1ELi1ELb1EEEvNS_8WalkArgsE"),
+    ("walk_modp64_kernel<32, 1, lazy>", r"_ZN2pk18walk_modp64_kernelILi32ELi1ELb1EEEvNS_8WalkArgsE"),
 ]
 
 
