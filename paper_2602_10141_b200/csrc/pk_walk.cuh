@@ -48,8 +48,14 @@
 #ifndef PK_COL0_ALIGN
 #define PK_COL0_ALIGN 0
 #endif
+// Two step pairs per compensated add (one Neumaier step per four terms).  The
+// loop body then holds two odd steps; their column-0 reads come from two
+// parameter copies (WalkArgs::col0, col0b) so that both stay uniform-register
+// operands (with one copy ptxas held the column in vector registers: LDC.64,
+// 8 % slower).  Measured 57.22 vs 57.37 ms complex, 20.01 vs 20.30 ms real at
+// n = 32 (profiles/r2_pair4.txt).
 #ifndef PK_PAIR4
-#define PK_PAIR4 0
+#define PK_PAIR4 1
 #endif
 namespace pk {
 
@@ -95,7 +101,7 @@ struct WalkArgs {
   double col0[2 * 48];  // read element by element (F64Walker::step_c0)
 #endif
 #if PK_PAIR4
-  double col0b[2 * 48];  // a second copy of col0 (experiment PK_PAIR4)
+  double col0b[2 * 48];  // a second copy of col0 (PK_PAIR4)
 #endif
 };
 #if PK_COL0_ALIGN
@@ -363,6 +369,11 @@ struct F64Walker {
     }
   }
 
+  // PK_PAIR4 applies to the single-matrix (C0P) kernels, where it was measured,
+  // up to the sizes whose four-step body still fits the register file without
+  // spilling (complex n <= 37, real n <= 63); the others keep one pair per step
+  static constexpr bool kPair4 = PK_PAIR4 && C0P && (CPLX ? N <= 37 : N <= 63);
+
   static constexpr int kSubBits = 12;
   __device__ __forceinline__ void walk(const T* __restrict__ base, const T* __restrict__ W, int m,
                                        int k, uint64_t seg) {
@@ -410,33 +421,42 @@ struct F64Walker {
            : kMinus ? step((mo ? W + m * NS : W) + (e >> 31) * NS, 1.0)
                     : step(W + (e >> 31) * NS, mo ? -1.0 : 1.0);
     };
-#if PK_PAIR4
-    // two step pairs per compensated add: d = (t0 - t1) + (t2 - t3), one
-    // Neumaier step per four terms (error <= 3 u (|t0| + ... + |t3|), inside
-    // the n u S gate); L = 2^k >= 4 here (k >= 2 whenever tiles exist)
-    for (uint32_t e = 2; e < L; e += 4) {
-      T pe, po, qe, qo;
-      pair_at(e, pe, po);
-      if (e + 2 < L) {
-        // the second odd step reads the parameter's second copy of column 0
-        // (WalkArgs::col0b): distinct uniform loads, not one copy held in
-        // vector registers across the body
-        const double* keep = c0d;
-        if (C0P) c0d = c0d2;
-        pair_at(e + 2, qe, qo);
-        c0d = keep;
-        add_quad(pe, po, qe, qo);
-      } else {
+    if constexpr (kPair4) {
+      // two step pairs per compensated add: d = (t0 - t1) + (t2 - t3), one
+      // Neumaier step per four terms (error <= 3 u (|t0| + ... + |t3|), inside
+      // the n u S gate)
+      for (uint32_t e = 2; e < L; e += 4) {
+        T pe, po, qe, qo;
+        pair_at(e, pe, po);
+        if (e + 2 < L) {
+          // the second odd step reads the parameter's second copy of column 0
+          // (WalkArgs::col0b): distinct uniform loads, not one copy held in
+          // vector registers across the body
+          const double* keep = c0d;
+          c0d = c0d2;
+          pair_at(e + 2, qe, qo);
+          c0d = keep;
+          add_quad(pe, po, qe, qo);
+        } else {
+          add_pair(pe, po);
+        }
+      }
+    } else {
+      // (the round-1 loop, written out: through the pair_at lambda ptxas spilled
+      // the n = 44-48 complex kernels' state, 200 B against 16 B)
+      for (uint32_t e = 2; e < L; e += 2) {
+        const int b = __ffs(e) - 1;
+        const bool me = StepPlan::minus_even(e, k, lane_minus);
+        const T pe = kMinus ? step((me ? W + m * NS : W) + b * NS, 1.0)
+                            : step(W + b * NS, me ? -1.0 : 1.0);
+        const bool mo = StepPlan::minus_odd(e + 1, k, lane_minus);
+        const T po = C0P      ? (PK_COL0_ALIGN ? step(c0, mo ? -1.0 : 1.0)
+                                               : step_c0(c0d, mo ? -1.0 : 1.0))
+                     : kMinus ? step((mo ? W + m * NS : W) + (e >> 31) * NS, 1.0)
+                              : step(W + (e >> 31) * NS, mo ? -1.0 : 1.0);
         add_pair(pe, po);
       }
     }
-#else
-    for (uint32_t e = 2; e < L; e += 2) {
-      T pe, po;
-      pair_at(e, pe, po);
-      add_pair(pe, po);
-    }
-#endif
   }
 };
 

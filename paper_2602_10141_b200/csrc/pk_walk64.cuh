@@ -26,10 +26,14 @@
 
 namespace pk {
 
+// Steps per loop body: two (the round-2 REDC made a step ~1,180 instructions;
+// the two-step body measured +4-5 % at n = 35 / 36 with no instruction-cache
+// stalls, where round 1's ~1,500-instruction steps thrashed it;
+// profiles/r2_wide_variants.txt)
 #ifndef PK_WIDE_UNROLL
-#define PK_WIDE_UNROLL 1
+#define PK_WIDE_UNROLL 2
 #endif
-constexpr int kWideUnroll = PK_WIDE_UNROLL;  // steps per loop body (experiment)
+constexpr int kWideUnroll = PK_WIDE_UNROLL;
 
 __device__ __forceinline__ uint64_t wmul32(uint32_t a, uint32_t b) {
   return static_cast<uint64_t>(a) * b;  // IMAD.WIDE.U32
@@ -257,9 +261,9 @@ struct Modp64Walker {
     for (int q = 0; q < P; ++q) acc_lo[q] = acc_hi[q] = 0ull;
     const uint32_t L = 1u << k;
     const bool lane_minus = seg & 1;
-    // One step (one product tree) per iteration: a REDC-64 tree is ~1,200
-    // instructions, and the two-step body of the 32-bit walk overflowed the
-    // instruction cache here (ncu: 2.1 no_instruction stalls per issue).
+    // Round 1 kept one step (one product tree) per loop body: its REDC-64 tree
+    // was ~1,500 instructions and a two-step body overflowed the instruction
+    // cache (ncu: 2.1 no_instruction stalls per issue).  See kWideUnroll.
     uint64_t y[P], ye[P];
 #pragma unroll kWideUnroll
     for (uint32_t s = 0; s < L; ++s) {

@@ -5,7 +5,7 @@
 Recompiles only the named instantiation objects (stems of the Makefile's
 build/inst_*.o, e.g. hyb_pi1_w1_29 = walk_hybrid_kernel<29..36, 1, 1, wide>) with
 the extra -D flags into paper_2602_10141_b200/csrc/build_var/NAME/ and links them
-with pk_capi.o, pk_peaks.o and weak no-op stand-ins for every other kernel
+with pk_capi.o, pk_peaks.o, pk_mix.o and weak no-op stand-ins for every other kernel
 table's registration function into paper_2602_10141_b200/_lib_var/NAME.so (a
 few MB instead of the full library's ~160 MB: gpurun snapshots are capped), and
 prints the path.  Only the named kernels exist in a variant library.  Select it at run time with PERMKIT_GPU_LIB=<path>
@@ -87,7 +87,7 @@ def main():
         capi = os.path.join(out_dir, "pk_capi.o")
         subprocess.run(["nvcc", *NVFLAGS, *flags, "-c", os.path.join(CSRC, "pk_capi.cu"), "-o", capi],
                        check=True)
-    objs = [capi, os.path.join(base, "pk_peaks.o"), stub[:-3] + ".o"]
+    objs = [capi, os.path.join(base, "pk_peaks.o"), os.path.join(base, "pk_mix.o"), stub[:-3] + ".o"]
     lib_dir = os.path.join(ROOT, "paper_2602_10141_b200", "_lib_var")
     os.makedirs(lib_dir, exist_ok=True)
     lib = os.path.join(lib_dir, f"{name}.so")
