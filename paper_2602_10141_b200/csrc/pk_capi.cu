@@ -1332,7 +1332,10 @@ extern "C" int pk_ryser_modp(const uint64_t* a, const uint64_t* primes, int P, i
         } else {
           const uint64_t s0 = start + static_cast<uint64_t>(static_cast<u128>(length) * d / ndev);
           const uint64_t s1 = start + static_cast<uint64_t>(static_cast<u128>(length) * (d + 1) / ndev);
-          const int bits = std::clamp(p.m - 17, 6, 62);
+          // pieces of <= 2^(m-17) indices, and at least ~2^14 of them so that a
+          // sub-range still fills the GPU (one thread walks one piece)
+          const int lb = s1 > s0 ? 63 - __builtin_clzll(s1 - s0) : 0;
+          const int bits = std::clamp(std::min(p.m - 17, lb - 14), 6, 62);
           split_pieces(s0, s1, bits, pcs);
         }
         if (pcs.empty()) continue;

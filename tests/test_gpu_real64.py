@@ -52,3 +52,92 @@ def test_real_limits(gpu):
         engine.perm_ryser(np.ones((64, 64)))
     with pytest.raises(LimitError):
         engine.perm_glynn(np.ones((49, 49), dtype=complex))
+
+
+
+def _sparse_sign_matrix(n, algo, cplx, seed):
+    """Entries in {0, +-1} (complex: {0, +-1, +-i}) with two nonzeros per row (Ryser's
+    row sums) or per column (Glynn's signed column sums): every state entry has
+    |r| <= 2, so every partial product of the walk is a (Gaussian) integer of modulus
+    <= 2^n -- exact in fp64 (real products are +-2^k; complex ones have components
+    < 2^53 for n <= 52)."""
+    rng = np.random.default_rng(seed)
+    a = np.zeros((n, n), dtype=complex if cplx else float)
+    for i in range(n):
+        for j in rng.choice(n, size=2, replace=False):
+            v = rng.choice([-1.0, 1.0]) * (1j if cplx and rng.random() < 0.5 else 1.0)
+            if algo == "ryser":
+                a[i, j] = v
+            else:
+                a[j, i] = v
+    return a
+
+
+def _primes_1mod4(count):
+    from paper_2602_10141_b200.modular import is_probable_prime
+    out, p = [], (1 << 31) - 3
+    while len(out) < count:
+        if p % 4 == 1 and is_probable_prime(p):
+            out.append(p)
+        p -= 2
+    return out
+
+
+def _sqrt_minus1(p):
+    c = 2
+    while pow(c, (p - 1) // 2, p) != p - 1:
+        c += 1
+    return pow(c, (p - 1) // 4, p)
+
+
+def _lift(residues, primes):
+    P = 1
+    for p in primes:
+        P *= p
+    x = 0
+    for r, p in zip(residues, primes):
+        q = P // p
+        x += r * q * pow(q, -1, p)
+    x %= P
+    return x - P if x > P // 2 else x
+
+
+@pytest.mark.parametrize("n,algo,cplx", [(40, "ryser", True), (44, "glynn", True),
+                                         (48, "ryser", False), (47, "glynn", False),
+                                         (56, "glynn", False), (63, "ryser", False)])
+def test_signed_integer_inputs_exact_at_max_sizes(gpu, monkeypatch, n, algo, cplx):
+    """A rigorous gate for SIGNED inputs at the largest n (the S-scaled tolerance of
+    the max-size tests is only rigorous for nonnegative inputs).  With
+    the sparse {0, +-1, +-i} matrices above every row sum and product of the walk is
+    exact, so the production fp64 walk's only error is its compensated summation.
+    The exact range sum E comes from the bit-exact F_p walks of the same range
+    (three primes p = 1 mod 4, i -> +-sqrt(-1) mod p separating Re and Im, CRT
+    lift).  Gate: |(s + c) - E| <= 2u|E| + 2^-70 S per component."""
+    from fractions import Fraction
+    monkeypatch.setenv("PK_PLAN_K", "12")
+    a = _sparse_sign_matrix(n, algo, cplx, n)
+    m = n if algo == "ryser" else n - 1
+    span = 64 << 17  # 64 tiles of 32 segments of 2^12 indices
+    st = int(np.random.default_rng(n + 1).integers(0, (1 << m) // span - 1)) * span
+    s, c, ab = gpu.ryser_f64(a, algo, st, span, want_abs=True)
+    primes = _primes_1mod4(3)
+    re_res, im_res = [], []
+    for p in primes:
+        g = _sqrt_minus1(p)
+        r = []
+        for gg in ((g, p - g) if cplx else (0,)):
+            mat = np.array([[(int(v.real) + int(v.imag) * gg) % p for v in row] for row in a],
+                           dtype=np.uint64)
+            r.append(gpu.ryser_modp(mat[None], [p], algo, st, span)[0])
+        if cplx:
+            inv2 = pow(2, -1, p)
+            re_res.append((r[0] + r[1]) * inv2 % p)
+            im_res.append((r[0] - r[1]) * inv2 * pow(g, -1, p) % p)
+        else:
+            re_res.append(r[0])
+    exact = [_lift(re_res, primes)] + ([_lift(im_res, primes)] if cplx else [])
+    got = [(complex(s).real, complex(c).real)] + ([(complex(s).imag, complex(c).imag)] if cplx else [])
+    for (gs, gc), E in zip(got, exact):
+        err = abs(Fraction(gs) + Fraction(gc) - E)
+        assert err <= 2 * Fraction(U) * abs(E) + Fraction(2) ** -70 * Fraction(ab), (n, algo, E)
+    assert any(E != 0 for E in exact)
