@@ -48,14 +48,15 @@
 #ifndef PK_COL0_ALIGN
 #define PK_COL0_ALIGN 0
 #endif
-// Two step pairs per compensated add (one Neumaier step per four terms).  The
-// loop body then holds two odd steps; their column-0 reads come from two
-// parameter copies (WalkArgs::col0, col0b) so that both stay uniform-register
-// operands (with one copy ptxas held the column in vector registers: LDC.64,
-// 8 % slower).  Measured 57.22 vs 57.37 ms complex, 20.01 vs 20.30 ms real at
-// n = 32 (profiles/r2_pair4.txt).
+// PK_PAIR4 (experiment, off): two step pairs per compensated add (one Neumaier
+// step per four terms).  The loop body then holds two odd steps; their column-0
+// reads come from two parameter copies (WalkArgs::col0, col0b) so both stay
+// uniform-register operands.  Measured 57.22 vs 57.37 ms complex, 20.01 vs
+// 20.30 ms real at n = 32 (profiles/r2_pair4.txt), but the batched
+// per-warp-slot kernels spill with the four-step body, and a pair-per-step
+// batch would no longer match a single call bit for bit: not adopted.
 #ifndef PK_PAIR4
-#define PK_PAIR4 1
+#define PK_PAIR4 0
 #endif
 namespace pk {
 
@@ -369,9 +370,8 @@ struct F64Walker {
     }
   }
 
-  // PK_PAIR4 applies to the single-matrix (C0P) kernels, where it was measured,
-  // up to the sizes whose four-step body still fits the register file without
-  // spilling (complex n <= 37, real n <= 63); the others keep one pair per step
+  // PK_PAIR4 only where the four-step body fits the register file without
+  // spilling (single-matrix kernels, complex n <= 37, real n <= 63)
   static constexpr bool kPair4 = PK_PAIR4 && C0P && (CPLX ? N <= 37 : N <= 63);
 
   static constexpr int kSubBits = 12;
