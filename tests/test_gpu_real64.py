@@ -55,22 +55,29 @@ def test_real_limits(gpu):
 
 
 
-def _sparse_sign_matrix(n, algo, cplx, seed):
-    """Entries in {0, +-1} (complex: {0, +-1, +-i}) with two nonzeros per row (Ryser's
-    row sums) or per column (Glynn's signed column sums): every state entry has
-    |r| <= 2, so every partial product of the walk is a (Gaussian) integer of modulus
-    <= 2^n -- exact in fp64 (real products are +-2^k; complex ones have components
-    < 2^53 for n <= 52)."""
+def _sparse_sign_matrix(n, cplx, seed):
+    """Ryser test matrix for an exact signed-input check (n even, L = n / 2 "low"
+    columns 0..L-1): row i has two nonzeros in {+-1} (complex: {+-1, +-i}), one in
+    a low and one in a high column, each column holding two (a random cycle through
+    alternately low and high columns).  Every row sum is in {0, +-1, +-i, +-2, ...}
+    with |r| <= 2, so every product of the walk is an exact (Gaussian) integer."""
     rng = np.random.default_rng(seed)
+    L = n // 2
+    low, high = rng.permutation(L), L + rng.permutation(n - L)
+    cyc = [c for pair in zip(low, high) for c in pair]  # low, high, low, high, ...
     a = np.zeros((n, n), dtype=complex if cplx else float)
     for i in range(n):
-        for j in rng.choice(n, size=2, replace=False):
-            v = rng.choice([-1.0, 1.0]) * (1j if cplx and rng.random() < 0.5 else 1.0)
-            if algo == "ryser":
-                a[i, j] = v
-            else:
-                a[j, i] = v
+        for j in (cyc[i], cyc[(i + 1) % n]):
+            a[i, j] = rng.choice([-1.0, 1.0]) * (1j if cplx and rng.random() < 0.5 else 1.0)
     return a
+
+
+def _gray_inverse(g):
+    b = 0
+    while g:
+        b ^= g
+        g >>= 1
+    return b
 
 
 def _primes_1mod4(count):
@@ -102,24 +109,28 @@ def _lift(residues, primes):
     return x - P if x > P // 2 else x
 
 
-@pytest.mark.parametrize("n,algo,cplx", [(40, "ryser", True), (44, "glynn", True),
-                                         (48, "ryser", False), (47, "glynn", False),
-                                         (56, "glynn", False), (63, "ryser", False)])
-def test_signed_integer_inputs_exact_at_max_sizes(gpu, monkeypatch, n, algo, cplx):
+@pytest.mark.parametrize("n,cplx", [(40, True), (44, True), (46, False), (48, False)])
+def test_signed_integer_inputs_exact_at_max_sizes(gpu, monkeypatch, n, cplx):
     """A rigorous gate for SIGNED inputs at the largest n (the S-scaled tolerance of
     the max-size tests is only rigorous for nonnegative inputs).  With
-    the sparse {0, +-1, +-i} matrices above every row sum and product of the walk is
-    exact, so the production fp64 walk's only error is its compensated summation.
-    The exact range sum E comes from the bit-exact F_p walks of the same range
-    (three primes p = 1 mod 4, i -> +-sqrt(-1) mod p separating Re and Im, CRT
-    lift).  Gate: |(s + c) - E| <= 2u|E| + 2^-70 S per component."""
+    the matrices above every row sum and product of the fp64 walk is exact, so the
+    production walk's only error is its compensated summation.  The range is the
+    aligned block of 2^L Gray indices whose high columns are all in the subset:
+    there every low column sits in two rows whose high parts h1, h2 are fixed, so the
+    range sum factorises into prod over low columns of -(h1 a2 + a1 h2 + a1 a2),
+    a nonzero integer (three units never cancel), reached through terms that cancel
+    in sign and through row sums that cancel (h + a = 0).  The exact value comes from
+    the bit-exact F_p walks of the same range (three primes p = 1 mod 4, i -> +-sqrt(-1)
+    mod p separating Re and Im, CRT lift).  Gate: |(s + c) - E| <= 2u|E| + 2^-70 S."""
     from fractions import Fraction
     monkeypatch.setenv("PK_PLAN_K", "12")
-    a = _sparse_sign_matrix(n, algo, cplx, n)
-    m = n if algo == "ryser" else n - 1
-    span = 64 << 17  # 64 tiles of 32 segments of 2^12 indices
-    st = int(np.random.default_rng(n + 1).integers(0, (1 << m) // span - 1)) * span
-    s, c, ab = gpu.ryser_f64(a, algo, st, span, want_abs=True)
+    a = _sparse_sign_matrix(n, cplx, n)
+    L = n // 2
+    high_mask = ((1 << n) - 1) ^ ((1 << L) - 1)
+    st = _gray_inverse(high_mask) & ~((1 << L) - 1)  # gray(st + t) has every high column
+    span = 1 << L
+    s, c, ab = gpu.ryser_f64(a, "ryser", st, span, want_abs=True)
+    assert ab > 0
     primes = _primes_1mod4(3)
     re_res, im_res = [], []
     for p in primes:
@@ -128,7 +139,7 @@ def test_signed_integer_inputs_exact_at_max_sizes(gpu, monkeypatch, n, algo, cpl
         for gg in ((g, p - g) if cplx else (0,)):
             mat = np.array([[(int(v.real) + int(v.imag) * gg) % p for v in row] for row in a],
                            dtype=np.uint64)
-            r.append(gpu.ryser_modp(mat[None], [p], algo, st, span)[0])
+            r.append(gpu.ryser_modp(mat[None], [p], "ryser", st, span)[0])
         if cplx:
             inv2 = pow(2, -1, p)
             re_res.append((r[0] + r[1]) * inv2 % p)
@@ -136,8 +147,9 @@ def test_signed_integer_inputs_exact_at_max_sizes(gpu, monkeypatch, n, algo, cpl
         else:
             re_res.append(r[0])
     exact = [_lift(re_res, primes)] + ([_lift(im_res, primes)] if cplx else [])
-    got = [(complex(s).real, complex(c).real)] + ([(complex(s).imag, complex(c).imag)] if cplx else [])
+    got = [(complex(s).real, complex(c).real)] + \
+        ([(complex(s).imag, complex(c).imag)] if cplx else [])
     for (gs, gc), E in zip(got, exact):
         err = abs(Fraction(gs) + Fraction(gc) - E)
-        assert err <= 2 * Fraction(U) * abs(E) + Fraction(2) ** -70 * Fraction(ab), (n, algo, E)
+        assert err <= 2 * Fraction(U) * abs(E) + Fraction(2) ** -70 * Fraction(ab), (n, E)
     assert any(E != 0 for E in exact)
