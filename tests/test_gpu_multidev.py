@@ -218,3 +218,17 @@ def test_perm_blocked_plan_vs_oracle(gpu):
     ref = oracle.permanent(a, "ryser", blocks=37)
     s, c, ab = gpu.ryser_f64(a, "ryser", 0, 1 << 18, want_abs=True)
     assert abs(got - ref) <= 8 * 18 * 2.0 ** -53 * ab + 4 * 2.0 ** -53 * abs(ref)
+
+
+def test_plan_call_errors_and_edges(gpu):
+    """pk_ryser_f64_plan: empty plans, zero-length blocks, out-of-range blocks."""
+    a = ensembles.sample_matrix("haar-u", 10, 1, 0)
+    out, ab = gpu.ryser_f64_plan(a, "ryser", [], [])
+    assert out.shape == (0, 4)
+    out, _ = gpu.ryser_f64_plan(a, "ryser", [0, 5, 5], [5, 0, (1 << 10) - 5])
+    assert np.all(out[1] == 0)
+    s, c = gpu.kahan_fold(out, True)
+    one = gpu.ryser_f64(a, "ryser", 0, 1 << 10)
+    assert abs((s + c) - (one[0] + one[1])) < 1e-12 * abs(one[0] + one[1]) + 1e-300
+    with pytest.raises(gpu.GpuError):
+        gpu.ryser_f64_plan(a, "ryser", [1000], [100])  # beyond 2^10

@@ -329,3 +329,11 @@ def test_kahan_fold_matches_kahan_accumulator():
             acc.add(complex(r[2], r[3]) if cplx else r[2])
         s, c = _native.kahan_fold(rows, cplx)
         assert s == acc.sum and c == acc.compensation
+
+
+def test_kahan_fold_empty():
+    import numpy as np
+
+    from paper_2602_10141_b200 import _native
+    assert _native.kahan_fold(np.zeros((0, 4)), True) == (0j, 0j)
+    assert _native.kahan_fold(np.zeros((0, 4)), False) == (0.0, 0.0)
