@@ -34,6 +34,9 @@ namespace pk {
 #define PK_WIDE_UNROLL 2
 #endif
 constexpr int kWideUnroll = PK_WIDE_UNROLL;
+#ifndef PK_REDC64_WIDE_E
+#define PK_REDC64_WIDE_E 0  // experiment: hi(m0 p0) from a wide multiply
+#endif
 
 __device__ __forceinline__ uint64_t wmul32(uint32_t a, uint32_t b) {
   return static_cast<uint64_t>(a) * b;  // IMAD.WIDE.U32
@@ -85,7 +88,12 @@ __device__ __forceinline__ uint64_t redc64_lazy(uint64_t x, uint64_t y, uint64_t
       // high 64 bits of m p = m1 p1 + (m1 p0 + m0 p1 + hi(m0 p0)) >> 32
       "mul.wide.u32 a, m1, p0;\n\t"
       "mul.wide.u32 b, m0, p1;\n\t"
+#if PK_REDC64_WIDE_E
+      "mul.wide.u32 w, m0, p0;\n\t"  // (w reused below) only its high word matters
+      "mov.b64 {s1, e}, w;\n\t"
+#else
       "mul.hi.u32 e, m0, p0;\n\t"
+#endif
       "mul.wide.u32 w, m1, p1;\n\t"
       "mov.b64 {a0, a1}, a;\n\t"
       "mov.b64 {b0, b1}, b;\n\t"
