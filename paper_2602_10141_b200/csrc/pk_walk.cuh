@@ -606,6 +606,13 @@ __device__ void stage_modp(uint32_t* sm, const uint32_t* a, const uint32_t* prim
   }
 }
 
+// Step pairs per loop body of the F_p walks (experiment switch; 1 = the
+// compiler's choice of one pair)
+#ifndef PK_MODP_UNROLL
+#define PK_MODP_UNROLL 1
+#endif
+constexpr int kModpUnroll = PK_MODP_UNROLL;
+
 __device__ __forceinline__ uint32_t addmod_red(uint32_t r, uint32_t c, uint32_t p) {
   const uint32_t v = r + c;
   return min(v, v - p);
@@ -738,6 +745,7 @@ struct ModpWalker {
     tree(ye);
     step(StepPlan::minus_odd(1, k, lane_minus) ? Wm : W2, yo);
     add_pair(ye, yo);
+#pragma unroll kModpUnroll
     for (uint32_t e = 2; e < L; e += 2) {
       const int b = __ffs(e) - 1;
       step((StepPlan::minus_even(e, k, lane_minus) ? Wm : W2) + b * CS, ye);

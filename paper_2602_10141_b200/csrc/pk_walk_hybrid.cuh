@@ -266,6 +266,7 @@ struct HybridWalker {
       fw.product(fo);
       pair();
     }
+#pragma unroll kModpUnroll
     for (uint32_t e = 2; e < L; e += 2) {
       const int b = __ffs(e) - 1;
       const bool me = StepPlan::minus_even(e, k, lane_minus);
