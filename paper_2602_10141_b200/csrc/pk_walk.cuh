@@ -334,6 +334,39 @@ struct F64Walker {
   // Terms of a step pair (even e, odd e+1) carry opposite signs: their
   // difference is formed in plain fp64 (one rounding, <= u (|t_e| + |t_o|))
   // and compensated-added once, halving the Neumaier work.
+  // PK_BLOCK_SUM (experiment): the pair differences of kBlockPairs consecutive
+  // pairs are summed plainly (error <= kBlockPairs u sum |t|, inside the n u S
+  // gate for kBlockPairs <= n) and compensated-added once per block
+#ifndef PK_BLOCK_SUM
+#define PK_BLOCK_SUM 0
+#endif
+  static constexpr uint32_t kBlockPairs = 8;
+  T pend;
+  __device__ __forceinline__ void add_pair_blk(T pe, T po, bool flush) {
+    if constexpr (!PK_BLOCK_SUM) {
+      add_pair(pe, po);
+      return;
+    }
+    const T d = sub2(pe, po);
+    if constexpr (CPLX) {
+      pend.x += d.x;
+      pend.y += d.y;
+      if (want_abs) abs_acc += (fabs(pe.x) + fabs(pe.y)) + (fabs(po.x) + fabs(po.y));
+      if (flush) {
+        neumaier(s_re, c_re, pend.x);
+        neumaier(s_im, c_im, pend.y);
+        pend = F::zero();
+      }
+    } else {
+      pend += d;
+      if (want_abs) abs_acc += fabs(pe) + fabs(po);
+      if (flush) {
+        neumaier(s_re, c_re, pend);
+        pend = F::zero();
+      }
+    }
+  }
+
   __device__ __forceinline__ void add_pair(T pe, T po) {
     const T d = sub2(pe, po);
 #ifdef PK_EXP_NOKAHAN  // micro-experiments only (tools/micro): plain sums
@@ -406,7 +439,8 @@ struct F64Walker {
       const bool mo = StepPlan::minus_odd(1, k, lane_minus);
       const T po = kMinus ? step((mo ? W + m * NS : W) + (start >> 63) * NS, 1.0)
                           : step(W + (start >> 63) * NS, mo ? -1.0 : 1.0);
-      add_pair(pe, po);
+      pend = F::zero();
+      add_pair_blk(pe, po, L == 2);
     }
     auto pair_at = [&](uint32_t e, T& pe, T& po) {
       const int b = __ffs(e) - 1;
@@ -454,7 +488,7 @@ struct F64Walker {
                                                : step_c0(c0d, mo ? -1.0 : 1.0))
                      : kMinus ? step((mo ? W + m * NS : W) + (e >> 31) * NS, 1.0)
                               : step(W + (e >> 31) * NS, mo ? -1.0 : 1.0);
-        add_pair(pe, po);
+        add_pair_blk(pe, po, ((e >> 1) & (kBlockPairs - 1)) == kBlockPairs - 1 || e + 2 >= L);
       }
     }
   }
