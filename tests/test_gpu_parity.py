@@ -602,3 +602,23 @@ def test_c5_geodesic_sweep_n20_vs_oracle(gpu):
         ref = oracle.permanent(a, blocks=64)
         s, c, ab = gpu.ryser_f64(a, "ryser", 0, 1 << 20, want_abs=True)
         assert abs(z - ref) <= 8 * 20 * U * ab + 4 * U * abs(ref), t
+
+
+def test_integration_md_ctypes_stub(gpu, tmp_path):
+    """The ctypes stub INTEGRATION.md §2 tells a permkit maintainer to add works as
+    written: its ryser_partial / ryser_partial_modp are bit-identical to the oracle
+    (and so to kernels.ryser_partial / ryser_partial_modp, kernels.py:415-438)."""
+    import re
+    from conftest import ROOT
+    text = (ROOT / "INTEGRATION.md").read_text()
+    code = re.search(r"## 2\. ctypes stub.*?```python\n(.*?)```", text, re.S).group(1)
+    code = code.replace('ctypes.CDLL("libpermkit_gpu.so")', f'ctypes.CDLL("{gpu.library_path()}")')
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    a = ensembles.sample_matrix("haar-u", 14, 9, 0)
+    s, c = ns["ryser_partial"](a, 1234, 3000)
+    rs, rc = oracle.block_partial(a, 1234, 3000)
+    assert bits_equal(s, rs) and bits_equal(c, rc)
+    p = modular.find_primes(14, max_bits=31).primes[0]
+    au = modular._root_matrix_u64(14, p, modular.primitive_nth_root(p, 14))
+    assert ns["ryser_partial_modp"](au, 77, 5000, p) == oracle.block_partial_modp(au, 77, 5000, p)
