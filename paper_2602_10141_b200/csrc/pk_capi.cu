@@ -85,6 +85,9 @@ static const Tables& tables() {
   register_wide_l1_p1_##lo(t.wide[1][1]);
     PK_FOR_EACH_RANGE(PK_REGW1)
 #undef PK_REGW1
+#if PK_WIDE_PMAX >= 2
+    register_wide_l1_p2_29(t.wide[1][2]);
+#endif
     return t;
   }();
   return t;

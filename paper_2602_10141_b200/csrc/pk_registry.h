@@ -34,7 +34,13 @@ PK_FOR_EACH_HYBRID_RANGE(PK_DECL_HYBRID)
 #undef PK_DECL_HYBRID
 // wide (2^31 <= p < 2^62, Montgomery-64) kernels: one prime per lane (two per
 // lane measured 20-30 % slower per prime: register pressure, profiles/r1_modp_rates_wide2.json)
-constexpr int kMaxPWide = 1;
+#ifndef PK_WIDE_PMAX
+#define PK_WIDE_PMAX 1  // experiment switch: 2 moduli per lane (variant builds)
+#endif
+constexpr int kMaxPWide = PK_WIDE_PMAX;
+#if PK_WIDE_PMAX >= 2
+void register_wide_l1_p2_29(const void** tbl);  // N = 29..36, p < 2^60
+#endif
 #define PK_DECL_WIDE1(lo, hi)                     \
   void register_wide_l0_p1_##lo(const void** tbl); \
   void register_wide_l1_p1_##lo(const void** tbl);
