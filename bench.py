@@ -22,6 +22,8 @@ Printed JSON (rank 0, one line):
               x SMs x the SM clock sampled during the timed region
   cpu_baseline  the C restatement of the reference kernel (oracle/) on all host
               cores, block-sampled (per-step cost is start-independent)
+  secondary.c4   perm(S_37) (the paper's first C4 size) through the public API,
+              golden-asserted, beside the paper's H100 time
   secondary.crt  the north_star target: exact perm(S_n) (odd n, default 35)
               through F_p walks + CRT on three prime bases (the GPU basis, the
               reference's 31-bit basis and its default 59-bit basis), each value
@@ -63,6 +65,7 @@ def parse():
     ap.add_argument("--n", type=int, default=N_HEAD)
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--crt-n", type=int, default=35)
+    ap.add_argument("--c4-n", type=int, default=37)
     return ap.parse_args()
 
 
@@ -383,6 +386,37 @@ def crt_section(args, nat, modular, sms, mhz, rank, world, pkdist, mix=None):
     return out
 
 
+# the paper's own C4 timings on one H100, minutes
+PAPER_C4_MIN = {37: 4.2, 39: 23.0, 41: 88.0, 43: 424.0}
+
+
+def c4_section(n, modular):
+    """secondary.c4: perm(S_n) for the first C4 size through the public API
+    (schur_permanent_fast: GPU basis, Glynn), asserted equal to the
+    reference-produced golden when tests/golden/schur_ref_large.json holds it,
+    beside the paper's H100 time for the same n."""
+    golden = None
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "schur_ref_large.json")) as f:
+            for row in json.load(f)["rows"]:
+                if row["n"] == n and row.get("value") is not None:
+                    golden = int(row["value"])
+    except OSError:
+        pass
+    t0 = time.perf_counter()
+    v, b, _ = modular.schur_permanent_fast(n)
+    dt = time.perf_counter() - t0
+    if golden is not None:
+        assert v == golden, f"perm(S_{n}): {v} != golden {golden}"
+    out = {"n": n, "value": str(v), "golden": str(golden) if golden is not None else None,
+           "primes": list(b.primes), "e2e_s": dt,
+           "prime_row_updates": len(b.primes) * n * 2.0 ** (n - 1)}
+    if n in PAPER_C4_MIN:
+        out["paper_h100_s"] = PAPER_C4_MIN[n] * 60
+        out["speedup_vs_paper_h100"] = PAPER_C4_MIN[n] * 60 / dt
+    return out
+
+
 def crt_cpu_baseline(n, bases):
     """The reference's F_p kernel (oracle restatement of kernels.py:250-290 with
     _mulmod kernels.py:229-247) on all host cores, same sampling recipe: 2^bits
@@ -564,6 +598,8 @@ def main():
     if not args.no_secondary:
         sec = {}
         sec["crt"] = crt_section(args, nat, modular, sms, mhz, rank, world, pkdist, mix)
+        if rank == 0 and world == 1 and args.c4_n:
+            sec["c4"] = c4_section(args.c4_n, modular)
         if rank == 0 and world == 1:
             sec.update(secondary_c2(nat))
         out["secondary"] = sec
