@@ -232,3 +232,27 @@ def test_plan_call_errors_and_edges(gpu):
     assert abs((s + c) - (one[0] + one[1])) < 1e-12 * abs(one[0] + one[1]) + 1e-300
     with pytest.raises(gpu.GpuError):
         gpu.ryser_f64_plan(a, "ryser", [1000], [100])  # beyond 2^10
+
+
+def test_concurrent_calls_from_host_threads(gpu):
+    """The reference calls its block kernels from a ThreadPoolExecutor
+    (engine.py:234-236); the C ABI is reentrant (per-device lock, per-thread error
+    state): eight threads mixing fp64 ranges, F_p walks and plans give exactly the
+    serial results."""
+    from concurrent.futures import ThreadPoolExecutor
+    a = ensembles.sample_matrix("haar-u", 18, 3, 0)
+    p = modular.find_primes(18, max_bits=31).primes[0]
+    au = modular._root_matrix_u64(18, p, modular.primitive_nth_root(p, 18))
+
+    def job(i):
+        st, ln = 1000 * i, (1 << 17) + 37 * i
+        f = gpu.ryser_f64(a, "ryser" if i % 2 else "glynn", st, ln)
+        r = gpu.ryser_modp(au[None], [p], "ryser", st, ln)[0]
+        pl, _ = gpu.ryser_f64_plan(a, "ryser", [st, st + ln // 2], [ln // 2, ln - ln // 2])
+        return f, r, pl.tobytes()
+
+    serial = [job(i) for i in range(24)]
+    with ThreadPoolExecutor(8) as pool:
+        par = list(pool.map(job, range(24)))
+    for (f1, r1, p1), (f2, r2, p2) in zip(serial, par):
+        assert _pair_bits(f1, f2) and r1 == r2 and p1 == p2
