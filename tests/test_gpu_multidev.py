@@ -245,7 +245,7 @@ def test_concurrent_calls_from_host_threads(gpu):
     au = modular._root_matrix_u64(18, p, modular.primitive_nth_root(p, 18))
 
     def job(i):
-        st, ln = 1000 * i, (1 << 17) + 37 * i
+        st, ln = 1000 * i, (1 << 15) + 37 * i
         f = gpu.ryser_f64(a, "ryser" if i % 2 else "glynn", st, ln)
         r = gpu.ryser_modp(au[None], [p], "ryser", st, ln)[0]
         pl, _ = gpu.ryser_f64_plan(a, "ryser", [st, st + ln // 2], [ln // 2, ln - ln // 2])
