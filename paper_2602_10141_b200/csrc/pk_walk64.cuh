@@ -56,8 +56,72 @@ __device__ __forceinline__ uint32_t hi32(uint64_t v) { return static_cast<uint32
 //         then added to m1 p1 (its low 64 bits equal lo64(x y): no borrow).
 // 8 IMAD.WIDE.U32 + 1 IMAD.HI.U32 + 2 IMAD (40 fmaheavy SMSP cycles per warp)
 // and 8 carry-chain ALU instructions.
+// Word-serial Montgomery (CIOS) with two 32-bit rounds and the same R = 2^64:
+// m_i = t_i (-p^-1) mod 2^32, T += m_i p, T >>= 32.  8 IMAD.WIDE + 2 IMAD (36
+// fmaheavy cycles against redc64_lazy's 40) and ~15 carry adds on the ALU pipe,
+// which has room.  Output in [0, 2p) for x y < p 2^64 (T + m p < 2^127 for
+// p < 2^62).  Measured +4-6 % over redc64_lazy's form at n = 32-36
+// (profiles/r2_wide_variants.txt): the default.
+#ifndef PK_REDC64_CIOS
+#define PK_REDC64_CIOS 1
+#endif
+__device__ __forceinline__ uint64_t redc64_cios(uint64_t x, uint64_t y, uint64_t p,
+                                                uint64_t pinv) {
+  uint64_t r;
+  asm("{\n\t"
+      ".reg .u32 x0, x1, y0, y1, p0, p1, q0, q1, t0, t1, t2, t3, m0, m1, z;\n\t"
+      ".reg .u32 a0, a1, b0, b1, c0, c1, d0, d1, h0, h1, s0, s1;\n\t"
+      ".reg .u64 lo, mid, hi, a, b, c, d;\n\t"
+      "mov.b64 {x0, x1}, %1;\n\t"
+      "mov.b64 {y0, y1}, %2;\n\t"
+      "mov.b64 {p0, p1}, %3;\n\t"
+      "mov.b64 {q0, q1}, %4;\n\t"
+      "neg.s32 q0, q0;\n\t"  // -p^-1 mod 2^32 from the positive inverse
+      // T = x y = (t3 t2 t1 t0)
+      "mul.wide.u32 lo, x0, y0;\n\t"
+      "mul.wide.u32 mid, x0, y1;\n\t"
+      "mad.wide.u32 mid, x1, y0, mid;\n\t"
+      "mul.wide.u32 hi, x1, y1;\n\t"
+      "mov.b64 {t0, t1}, lo;\n\t"
+      "mov.b64 {s0, s1}, mid;\n\t"
+      "mov.b64 {h0, h1}, hi;\n\t"
+      "add.cc.u32 t1, t1, s0;\n\t"
+      "addc.cc.u32 t2, h0, s1;\n\t"
+      "addc.u32 t3, h1, 0;\n\t"
+      // round 1: T += m0 p, drop t0
+      "mul.lo.u32 m0, t0, q0;\n\t"
+      "mul.wide.u32 a, m0, p0;\n\t"
+      "mul.wide.u32 b, m0, p1;\n\t"
+      "mov.b64 {a0, a1}, a;\n\t"
+      "mov.b64 {b0, b1}, b;\n\t"
+      "add.cc.u32 z, t0, a0;\n\t"  // 0 mod 2^32: only the carry
+      "addc.cc.u32 t1, t1, a1;\n\t"
+      "addc.cc.u32 t2, t2, 0;\n\t"
+      "addc.u32 t3, t3, 0;\n\t"
+      "add.cc.u32 t1, t1, b0;\n\t"
+      "addc.cc.u32 t2, t2, b1;\n\t"
+      "addc.u32 t3, t3, 0;\n\t"
+      // round 2: T += m1 p 2^32, drop t1
+      "mul.lo.u32 m1, t1, q0;\n\t"
+      "mul.wide.u32 c, m1, p0;\n\t"
+      "mul.wide.u32 d, m1, p1;\n\t"
+      "mov.b64 {c0, c1}, c;\n\t"
+      "mov.b64 {d0, d1}, d;\n\t"
+      "add.cc.u32 z, t1, c0;\n\t"
+      "addc.cc.u32 t2, t2, c1;\n\t"
+      "addc.u32 t3, t3, 0;\n\t"
+      "add.cc.u32 t2, t2, d0;\n\t"
+      "addc.u32 t3, t3, d1;\n\t"
+      "mov.b64 %0, {t2, t3};\n\t"
+      "}"
+      : "=l"(r)
+      : "l"(x), "l"(y), "l"(p), "l"(pinv));
+  return r;
+}
+
 __device__ __forceinline__ uint64_t redc64_lazy(uint64_t x, uint64_t y, uint64_t p,
                                                 uint64_t pinv) {
+  if constexpr (PK_REDC64_CIOS) return redc64_cios(x, y, p, pinv);
   // one PTX block: left to the front end, the 64-bit adds of zero-extended
   // words survived as VIADD-with-zero register copies (~5 per REDC)
   uint64_t r;
