@@ -53,13 +53,13 @@ KERNELS = {
     "hybw_36": ("_ZN2pk18walk_hybrid_kernelILi36ELi1ELi1ELb1EEEvNS_8WalkArgsE", "inst_hyb_pi1_w1_29.o",
                 36, 2, "IMAD.HI.U32", 35, "walk_hybrid_kernel<36, 1 lazy + 1 wide fp64 prime>"),
     "wide_35": ("_ZN2pk18walk_modp64_kernelILi35ELi1ELb1EEEvNS_8WalkArgsE", "inst_wide_l1_p1_29.o",
-                35, 1, ("IMAD.WIDE.U32", "IMAD.HI.U32"), None,
+                35, 1, "IMAD.WIDE.U32", None,
                 "walk_modp64_kernel<35, 1 prime, lazy rows> (Montgomery-64, p < 2^60)"),
     "wide_36": ("_ZN2pk18walk_modp64_kernelILi36ELi1ELb1EEEvNS_8WalkArgsE", "inst_wide_l1_p1_29.o",
-                36, 1, ("IMAD.WIDE.U32", "IMAD.HI.U32"), None,
+                36, 1, "IMAD.WIDE.U32", None,
                 "walk_modp64_kernel<36, 1 prime, lazy rows> (Montgomery-64, p < 2^60)"),
     "wide62_36": ("_ZN2pk18walk_modp64_kernelILi36ELi1ELb0EEEvNS_8WalkArgsE", "inst_wide_l0_p1_29.o",
-                  36, 1, ("IMAD.WIDE.U32", "IMAD.HI.U32"), None,
+                  36, 1, "IMAD.WIDE.U32", None,
                   "walk_modp64_kernel<36, 1 prime, reduced rows> (Montgomery-64, p < 2^62)"),
 }
 
@@ -139,8 +139,8 @@ def analyse(tag, spec, listings):
     rows = parse(sass(mangled, obj))
     if not rows:
         raise SystemExit(f"{tag}: {mangled} not found in {obj} (build first)")
-    if per_step is None:  # Montgomery-64: 9 IMAD.WIDE / IMAD.HI per REDC, n - 1 REDCs per step
-        per_step = 9 * (n - 1)
+    if per_step is None:  # Montgomery-64: 8 IMAD.WIDE per REDC, n - 1 REDCs per step
+        per_step = 8 * (n - 1)
     loop, mk = hot_loop(rows, marker, per_step)
     counts = collections.Counter(opcode(i) for _, i in loop)
     steps = round(mk / per_step)
