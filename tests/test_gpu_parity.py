@@ -487,6 +487,17 @@ def test_schur_resumable_checkpoint(gpu, tmp_path):
     assert done == 4 and v == -5198937484375
 
 
+def test_schur_resumable_rank_files(gpu, tmp_path):
+    """Two scheduler-given ranks on one GPU, exchanging finished chunks through their files."""
+    ck = str(tmp_path / "s25.jsonl")
+    v, _, _, done = modular.schur_permanent_resumable(25, ck, chunks=8, rank=1, world=2)
+    assert v is None and done == 4
+    v, _, _, done = modular.schur_permanent_resumable(25, ck, chunks=8, rank=0, world=2)
+    assert done == 8 and v == -5198937484375
+    v, _, _, done = modular.schur_permanent_resumable(25, ck, chunks=8)  # world 1 resumes
+    assert done == 8 and v == -5198937484375
+
+
 @pytest.mark.parametrize("fkind", ["fp64", "fp64w"])
 def test_hybrid_fp64_primes_vs_oracle(gpu, fkind):
     """Montgomery + fp64 primes walked together (hybrid kernel) are exact, for the

@@ -1,6 +1,10 @@
 """perm(S_45) exactly on one B200, on two independent prime bases (checkpointed).
 
     python tools/schur45.py  -> gpurun_out/schur45.json, gpurun_out/s45_*.jsonl checkpoints
+    torchrun --nproc-per-node 8 --master-addr 127.0.0.1 tools/schur45.py   (one rank per GPU)
+Under torchrun each rank walks chunks c = rank (mod world) on its own GPU
+(set_device_base(LOCAL_RANK)), writes s45_*.jsonl.rank<r>, and the residues are
+gathered over a gloo group; a rerun with any world size resumes from all the files.
 The paper projects ~28 GPU-hours for n = 45.
 """
 import json
@@ -9,13 +13,15 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2602_10141_b200 import modular  # noqa: E402
+from paper_2602_10141_b200 import _native, modular  # noqa: E402
+
+CHUNKS = 64  # 2^44 / 64 = 2^38 Glynn indices per chunk: 8 ranks get 8 chunks each
 
 
 def run(tag, basis):
     t0 = time.perf_counter()
-    v, b, w, done = modular.schur_permanent_resumable(45, f"gpurun_out/s45_{tag}.jsonl", chunks=16,
-                                                      basis=basis)
+    v, b, w, done = modular.schur_permanent_resumable(45, f"gpurun_out/s45_{tag}.jsonl",
+                                                      chunks=CHUNKS, basis=basis)
     return {"basis": list(b.primes), "value": str(v), "chunks_done": done,
             "residues": [x.residue for x in w] if w else None,
             "wall_s": time.perf_counter() - t0}
@@ -23,15 +29,21 @@ def run(tag, basis):
 
 def main():
     os.makedirs("gpurun_out", exist_ok=True)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        _native.set_device_base(int(os.environ.get("LOCAL_RANK", "0")))
     out = {"n": 45, "expansion": "glynn"}
     out["fast"] = run("fast", modular.gpu_prime_basis(45))
     print(json.dumps(out["fast"]), flush=True)
     out["check31"] = run("check31", modular.find_primes(45, max_bits=31))
     print(json.dumps(out["check31"]), flush=True)
     out["agree"] = out["fast"]["value"] == out["check31"]["value"]
-    with open("gpurun_out/schur45.json", "w") as f:
-        json.dump(out, f, indent=1)
-    print("agree:", out["agree"])
+    if int(os.environ.get("RANK", "0")) == 0:
+        with open("gpurun_out/schur45.json", "w") as f:
+            json.dump(out, f, indent=1)
+        print("agree:", out["agree"])
 
 
 if __name__ == "__main__":
