@@ -48,11 +48,20 @@ __device__ __forceinline__ void neumaier_ref(double& s, double& c, double v) {
   s = t;
 }
 
+// steps in flight per thread (block_f64_kernel / block_modp_kernel skewed passes)
+constexpr int block_skew(bool cplx, int nmax) { return !cplx ? 4 : nmax >= 64 ? 1 : nmax >= 48 ? 2 : 4; }
+
 __device__ __forceinline__ int ctz64(uint64_t x) { return __ffsll(static_cast<long long>(x)) - 1; }
+
+// The state r[] is indexed only by unrolled loop counters below NMAX (guarded by
+// i < n), so it lives in registers: NMAX is the smallest of 16 / 32 / 48 / 64 that
+// holds n (block_nmax).  Skipped iterations do no arithmetic, so the operation
+// sequence, and with it every bit, is the reference's for any NMAX >= n.
+#define PK_FOR_ROWS(i) _Pragma("unroll") for (int i = 0; i < NMAX; ++i) if (i < n)
 
 // out[blk * 4 + {0,1,2,3}] = (s_re, s_im, c_re, c_im); block blk walks matrix
 // a + (blk / ppm) * mat_stride (ppm = nblocks, stride 0: one matrix)
-template <bool CPLX, int ALGO>
+template <bool CPLX, int ALGO, int NMAX>
 __global__ void __launch_bounds__(kBlockThreads) block_f64_kernel(const double* __restrict__ a,
                                                                   int n,
                                                                   const uint64_t* __restrict__ starts,
@@ -63,7 +72,7 @@ __global__ void __launch_bounds__(kBlockThreads) block_f64_kernel(const double* 
   const int blk = blockIdx.x * blockDim.x + threadIdx.x;
   if (blk >= nblocks) return;
   a += static_cast<size_t>(blk / ppm) * mat_stride;  // ppm blocks per matrix (batched pieces)
-  C2 r[kBlockMaxN];
+  C2 r[NMAX];
   double abs_acc = 0.0;
   auto A = [&](int i, int j) -> C2 {
     if constexpr (CPLX) return C2{a[2 * (i * n + j)], a[2 * (i * n + j) + 1]};
@@ -73,11 +82,11 @@ __global__ void __launch_bounds__(kBlockThreads) block_f64_kernel(const double* 
   uint64_t g = start ^ (start >> 1);
   int pop = 0;
   if constexpr (ALGO == 0) {
-    for (int i = 0; i < n; ++i) r[i] = C2{0.0, 0.0};
+    PK_FOR_ROWS(i) r[i] = C2{0.0, 0.0};
     for (int j = 0; j < n; ++j) {
       if ((g >> j) & 1) {
         ++pop;
-        for (int i = 0; i < n; ++i) {
+        PK_FOR_ROWS(i) {
           const C2 x = A(i, j);
           r[i].re = __dadd_rn(r[i].re, x.re);
           if constexpr (CPLX) r[i].im = __dadd_rn(r[i].im, x.im);
@@ -85,11 +94,11 @@ __global__ void __launch_bounds__(kBlockThreads) block_f64_kernel(const double* 
       }
     }
   } else {
-    for (int j = 0; j < n; ++j) r[j] = A(0, j);
+    PK_FOR_ROWS(j) r[j] = A(0, j);
     for (int i = 0; i < n - 1; ++i) {
       const bool on = (g >> i) & 1;
       pop += on;
-      for (int j = 0; j < n; ++j) {
+      PK_FOR_ROWS(j) {
         const C2 x = A(i + 1, j);
         if (on) {
           r[j].re = __dsub_rn(r[j].re, x.re);
@@ -104,16 +113,77 @@ __global__ void __launch_bounds__(kBlockThreads) block_f64_kernel(const double* 
   int neg = ALGO == 0 ? ((n - pop) & 1) : (pop & 1);
   double s_re = 0.0, c_re = 0.0, s_im = 0.0, c_im = 0.0;
   uint64_t idx = start;
-  for (uint64_t step = 0; step < length; ++step) {
+  uint64_t step = 0;
+  // KS steps per pass, skewed: at row i, chain k multiplies row i of step + k and
+  // then moves that row to step + k + 1, which is exactly what chain k + 1 reads
+  // next.  Each step's product and update sequence is unchanged (bit-identical),
+  // but KS independent product chains are in flight instead of one.
+  constexpr int KS = block_skew(CPLX, NMAX);
+  for (; KS > 1 && step + KS < length; step += KS) {
+    int bk[KS];
+    bool sk[KS];
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      bk[k] = ctz64(++idx);
+      sk[k] = (g >> bk[k]) & 1;
+      g ^= 1ull << bk[k];
+    }
+    C2 pr[KS];
+#pragma unroll
+    for (int k = 0; k < KS; ++k) pr[k] = C2{1.0, 0.0};
+    PK_FOR_ROWS(i) {
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        if constexpr (CPLX)
+          pr[k] = cmul_ref(pr[k], r[i]);
+        else
+          pr[k].re = __dmul_rn(pr[k].re, r[i].re);
+        if constexpr (ALGO == 0) {
+          const C2 x = A(i, bk[k]);
+          if (sk[k]) {
+            r[i].re = __dsub_rn(r[i].re, x.re);
+            if constexpr (CPLX) r[i].im = __dsub_rn(r[i].im, x.im);
+          } else {
+            r[i].re = __dadd_rn(r[i].re, x.re);
+            if constexpr (CPLX) r[i].im = __dadd_rn(r[i].im, x.im);
+          }
+        } else {
+          const C2 x = A(bk[k] + 1, i);
+          C2 two;
+          if constexpr (CPLX)
+            two = cmul_ref(C2{2.0, 0.0}, x);
+          else
+            two = C2{__dmul_rn(2.0, x.re), 0.0};
+          if (sk[k]) {
+            r[i].re = __dadd_rn(r[i].re, two.re);
+            if constexpr (CPLX) r[i].im = __dadd_rn(r[i].im, two.im);
+          } else {
+            r[i].re = __dsub_rn(r[i].re, two.re);
+            if constexpr (CPLX) r[i].im = __dsub_rn(r[i].im, two.im);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      const double v_re = neg ? -pr[k].re : pr[k].re;
+      const double v_im = CPLX ? (neg ? -pr[k].im : pr[k].im) : 0.0;
+      neumaier_ref(s_re, c_re, v_re);
+      if constexpr (CPLX) neumaier_ref(s_im, c_im, v_im);
+      if (abs_out) abs_acc += fabs(v_re) + fabs(v_im);
+      neg ^= 1;
+    }
+  }
+  for (; step < length; ++step) {
     double v_re, v_im = 0.0;
     if constexpr (CPLX) {
       C2 prod{1.0, 0.0};
-      for (int i = 0; i < n; ++i) prod = cmul_ref(prod, r[i]);
+      PK_FOR_ROWS(i) prod = cmul_ref(prod, r[i]);
       v_re = neg ? -prod.re : prod.re;
       v_im = neg ? -prod.im : prod.im;
     } else {
       double prod = 1.0;
-      for (int i = 0; i < n; ++i) prod = __dmul_rn(prod, r[i].re);
+      PK_FOR_ROWS(i) prod = __dmul_rn(prod, r[i].re);
       v_re = neg ? -prod : prod;
     }
     neumaier_ref(s_re, c_re, v_re);
@@ -124,7 +194,7 @@ __global__ void __launch_bounds__(kBlockThreads) block_f64_kernel(const double* 
       const int b = ctz64(idx);
       const bool set = (g >> b) & 1;
       if constexpr (ALGO == 0) {
-        for (int i = 0; i < n; ++i) {
+        PK_FOR_ROWS(i) {
           const C2 x = A(i, b);
           if (set) {
             r[i].re = __dsub_rn(r[i].re, x.re);
@@ -135,7 +205,7 @@ __global__ void __launch_bounds__(kBlockThreads) block_f64_kernel(const double* 
           }
         }
       } else {
-        for (int j = 0; j < n; ++j) {
+        PK_FOR_ROWS(j) {
           const C2 x = A(b + 1, j);
           C2 two;
           if constexpr (CPLX)
@@ -161,6 +231,9 @@ __global__ void __launch_bounds__(kBlockThreads) block_f64_kernel(const double* 
   out[4 * blk + 3] = c_im;
   if (abs_out) abs_out[blk] = abs_acc;
 }
+
+// smallest register-state bound that holds n (n <= kBlockMaxN)
+inline int block_nmax(int n) { return n <= 16 ? 16 : n <= 32 ? 32 : n <= 48 ? 48 : 64; }
 
 // ---------------------------------------------------------------------------
 // F_p blocks, any modulus 2 <= p < 2^62.
@@ -190,7 +263,7 @@ struct ModArith {
 // Montgomery scale 2^(-64 (n-1)) for odd p (the host multiplies by 2^(64(n-1))),
 // and plain for even p.  Glynn's 2^(1-n) is applied by the caller, as in the
 // reference engine (engine.py:252-258).
-template <int ALGO>
+template <int ALGO, int NMAX>
 __global__ void __launch_bounds__(kBlockThreads) block_modp_kernel(const uint64_t* __restrict__ a,
                                                                    int n, uint64_t p,
                                                                    const uint64_t* __restrict__ starts,
@@ -199,23 +272,23 @@ __global__ void __launch_bounds__(kBlockThreads) block_modp_kernel(const uint64_
   const int blk = blockIdx.x * blockDim.x + threadIdx.x;
   if (blk >= nblocks) return;
   ModArith ar{p, (p & 1) ? mont_neg_inv64(p) : 0ull, (p & 1) != 0};
-  uint64_t r[kBlockMaxN];
+  uint64_t r[NMAX];
   const uint64_t start = starts[blk], length = lens[blk];
   uint64_t g = start ^ (start >> 1);
   int pop = 0;
   if constexpr (ALGO == 0) {
-    for (int i = 0; i < n; ++i) r[i] = 0;
+    PK_FOR_ROWS(i) r[i] = 0;
     for (int j = 0; j < n; ++j)
       if ((g >> j) & 1) {
         ++pop;
-        for (int i = 0; i < n; ++i) r[i] = ar.add(r[i], a[i * n + j]);
+        PK_FOR_ROWS(i) r[i] = ar.add(r[i], a[i * n + j]);
       }
   } else {
-    for (int j = 0; j < n; ++j) r[j] = a[j];
+    PK_FOR_ROWS(j) r[j] = a[j];
     for (int i = 0; i < n - 1; ++i) {
       const bool on = (g >> i) & 1;
       pop += on;
-      for (int j = 0; j < n; ++j) {
+      PK_FOR_ROWS(j) {
         const uint64_t x = a[(i + 1) * n + j];
         r[j] = ar.add(r[j], on ? ar.neg(x) : x);
       }
@@ -224,21 +297,53 @@ __global__ void __launch_bounds__(kBlockThreads) block_modp_kernel(const uint64_
   int neg = ALGO == 0 ? ((n - pop) & 1) : (pop & 1);
   uint64_t acc = 0;
   uint64_t idx = start;
-  for (uint64_t step = 0; step < length; ++step) {
+  uint64_t step = 0;
+  constexpr int KS = block_skew(false, NMAX);  // skewed passes, as in block_f64_kernel
+  for (; step + KS < length; step += KS) {
+    int bk[KS];
+    bool sk[KS];
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      bk[k] = ctz64(++idx);
+      sk[k] = (g >> bk[k]) & 1;
+      g ^= 1ull << bk[k];
+    }
+    uint64_t pr[KS];
+    PK_FOR_ROWS(i) {
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        pr[k] = i == 0 ? r[0] : ar.mul(pr[k], r[i]);
+        if constexpr (ALGO == 0) {
+          const uint64_t x = a[i * n + bk[k]];
+          r[i] = ar.add(r[i], sk[k] ? ar.neg(x) : x);
+        } else {
+          const uint64_t x = a[(bk[k] + 1) * n + i];
+          const uint64_t two = ar.add(x, x);
+          r[i] = ar.add(r[i], sk[k] ? two : ar.neg(two));
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      acc = ar.add(acc, neg ? ar.neg(pr[k]) : pr[k]);
+      neg ^= 1;
+    }
+  }
+  for (; step < length; ++step) {
     uint64_t prod = r[0];
-    for (int i = 1; i < n; ++i) prod = ar.mul(prod, r[i]);
+    _Pragma("unroll") for (int i = 1; i < NMAX; ++i) if (i < n) prod = ar.mul(prod, r[i]);
     acc = ar.add(acc, neg ? ar.neg(prod) : prod);
     if (step + 1 < length) {
       ++idx;
       const int b = ctz64(idx);
       const bool set = (g >> b) & 1;
       if constexpr (ALGO == 0) {
-        for (int i = 0; i < n; ++i) {
+        PK_FOR_ROWS(i) {
           const uint64_t x = a[i * n + b];
           r[i] = ar.add(r[i], set ? ar.neg(x) : x);
         }
       } else {
-        for (int j = 0; j < n; ++j) {
+        PK_FOR_ROWS(j) {
           const uint64_t x = a[(b + 1) * n + j];
           const uint64_t two = ar.add(x, x);
           r[j] = ar.add(r[j], set ? two : ar.neg(two));
@@ -250,5 +355,7 @@ __global__ void __launch_bounds__(kBlockThreads) block_modp_kernel(const uint64_
   }
   out[blk] = acc;
 }
+
+#undef PK_FOR_ROWS
 
 }  // namespace pk

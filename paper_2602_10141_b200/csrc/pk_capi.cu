@@ -479,19 +479,27 @@ static std::vector<Node> run_f64_pieces(DevCtx& c, const double* d_a, int n, boo
   PK_CUDA(cudaMemcpyAsync(dl, hl.data(), np * 8, cudaMemcpyHostToDevice, c.stream));
   const int grid = (np + kBlockThreads - 1) / kBlockThreads;
   double* ab = want_abs ? dabs : nullptr;
-#define PK_BLOCK(C, A) \
-  block_f64_kernel<C, A><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab, ppm, mat_stride)
+#define PK_BLOCK(C, A, NM) \
+  block_f64_kernel<C, A, NM><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, ds, dl, np, dout, ab, ppm, mat_stride)
+#define PK_BLOCK_N(C, A)                \
+  switch (block_nmax(n)) {              \
+    case 16: PK_BLOCK(C, A, 16); break; \
+    case 32: PK_BLOCK(C, A, 32); break; \
+    case 48: PK_BLOCK(C, A, 48); break; \
+    default: PK_BLOCK(C, A, 64); break; \
+  }
   if (cplx) {
     if (algo == 0)
-      PK_BLOCK(true, 0);
+      PK_BLOCK_N(true, 0)
     else
-      PK_BLOCK(true, 1);
+      PK_BLOCK_N(true, 1)
   } else {
     if (algo == 0)
-      PK_BLOCK(false, 0);
+      PK_BLOCK_N(false, 0)
     else
-      PK_BLOCK(false, 1);
+      PK_BLOCK_N(false, 1)
   }
+#undef PK_BLOCK_N
 #undef PK_BLOCK
   PK_CUDA(cudaGetLastError());
   std::vector<double> h(np * 4), habs(np, 0.0);
@@ -1116,10 +1124,20 @@ static uint64_t modp_pieces(DevCtx& c, const uint64_t* d_a, int n, int algo, uin
   PK_CUDA(cudaMemcpyAsync(ds, hs.data(), np * 8, cudaMemcpyHostToDevice, c.stream));
   PK_CUDA(cudaMemcpyAsync(dl, hl.data(), np * 8, cudaMemcpyHostToDevice, c.stream));
   const int grid = (np + kBlockThreads - 1) / kBlockThreads;
+#define PK_BLOCKP(A, NM) block_modp_kernel<A, NM><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, p, ds, dl, np, dout)
+#define PK_BLOCKP_N(A)                \
+  switch (block_nmax(n)) {            \
+    case 16: PK_BLOCKP(A, 16); break; \
+    case 32: PK_BLOCKP(A, 32); break; \
+    case 48: PK_BLOCKP(A, 48); break; \
+    default: PK_BLOCKP(A, 64); break; \
+  }
   if (algo == 0)
-    block_modp_kernel<0><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, p, ds, dl, np, dout);
+    PK_BLOCKP_N(0)
   else
-    block_modp_kernel<1><<<grid, kBlockThreads, 0, c.stream>>>(d_a, n, p, ds, dl, np, dout);
+    PK_BLOCKP_N(1)
+#undef PK_BLOCKP_N
+#undef PK_BLOCKP
   PK_CUDA(cudaGetLastError());
   PK_CUDA(cudaMemcpyAsync(ho.data(), dout, np * 8, cudaMemcpyDeviceToHost, c.stream));
   PK_CUDA(cudaStreamSynchronize(c.stream));

@@ -51,6 +51,29 @@ def test_exact_kernel_bit_identical_to_reference_blocks(gpu):
     assert checked >= 80
 
 
+@pytest.mark.parametrize("n", [5, 16, 17, 33, 48, 49, 64])
+def test_exact_kernel_every_state_bound_and_skew_tail(gpu, n):
+    """The block kernel's register-state bounds (NMAX 16/32/48/64) and its skewed passes
+    (4 or 2 steps in flight, csrc/pk_block.cuh): every block length 1..9 (tails shorter
+    than, equal to and just past a pass) and two long ones, bit-identical to the oracle's
+    restatement of kernels.py:33-226."""
+    rng = np.random.default_rng(n)
+    for cplx in (False, True):
+        a = rng.standard_normal((n, n))
+        if cplx:
+            a = a + 1j * rng.standard_normal((n, n))
+        for algo in ("ryser", "glynn"):
+            m = n if algo == "ryser" else n - 1
+            lens = [ln for ln in list(range(1, 10)) + [517, 1024] if ln < (1 << m)]
+            starts = [int(rng.integers(0, (1 << min(m, 62)) - ln + 1)) for ln in lens]
+            out = gpu.ryser_f64_blocks(a, algo, starts, lens)
+            for st, ln, row in zip(starts, lens, out):
+                ws, wc = oracle.block_partial(a, st, ln, algo)
+                gs = complex(row[0], row[1]) if cplx else float(row[0])
+                gc = complex(row[2], row[3]) if cplx else float(row[2])
+                assert bits_equal(gs, ws) and bits_equal(gc, wc), (cplx, algo, n, st, ln)
+
+
 def test_production_kernel_blocks_vs_exact(gpu):
     """Production path on every golden block, gated against the EXACT block sum.
 
@@ -232,6 +255,21 @@ def test_modp_blocks_bit_exact(gpu):
         fn = kernels.ryser_partial_modp if case["algorithm"] == "ryser" else kernels.glynn_partial_modp
         for b in case["blocks"]:
             assert fn(a, b["start"], b["len"], case["p"]) == b["res"], (case["n"], case["p"], b)
+
+
+@pytest.mark.parametrize("n", [7, 17, 33, 49])
+def test_modp_blocks_every_state_bound_and_skew_tail(gpu, n):
+    """F_p block kernel: NMAX buckets and skewed-pass tails (lengths 1..9), odd and even p."""
+    rng = np.random.default_rng(100 + n)
+    for p in (1000003, 4294967311, (1 << 61) - 1, 1 << 40, 999999999990):
+        a = rng.integers(0, p, (n, n), dtype=np.uint64)
+        for algo in ("ryser", "glynn"):
+            m = n if algo == "ryser" else n - 1
+            fn = kernels.ryser_partial_modp if algo == "ryser" else kernels.glynn_partial_modp
+            for ln in [x for x in list(range(1, 10)) + [301] if x < (1 << m)]:
+                st = int(rng.integers(0, (1 << m) - ln + 1))
+                assert fn(a, st, ln, p) == oracle.block_partial_modp(a, st, ln, p, algo), \
+                    (n, p, algo, st, ln)
 
 
 def test_modp_random_blocks_vs_oracle_large_n(gpu):
