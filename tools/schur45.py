@@ -15,12 +15,13 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_10141_b200 import _native, modular  # noqa: E402
 
+CKDIR = os.environ.get("S45_CKDIR", "gpurun_out")  # copy checkpoints here to resume a cut run
 CHUNKS = 64  # 2^44 / 64 = 2^38 Glynn indices per chunk: 8 ranks get 8 chunks each
 
 
 def run(tag, basis):
     t0 = time.perf_counter()
-    v, b, w, done = modular.schur_permanent_resumable(45, f"gpurun_out/s45_{tag}.jsonl",
+    v, b, w, done = modular.schur_permanent_resumable(45, os.path.join(CKDIR, f"s45_{tag}.jsonl"),
                                                       chunks=CHUNKS, basis=basis)
     return {"basis": list(b.primes), "value": str(v), "chunks_done": done,
             "residues": [x.residue for x in w] if w else None,
