@@ -525,6 +525,32 @@ def test_schur_resumable_checkpoint(gpu, tmp_path):
     assert done == 4 and v == -5198937484375
 
 
+@pytest.mark.parametrize("tag,chunk", [("fast", 63), ("check31", 17)])
+def test_schur45_chunk_replay(gpu, tmp_path, tag, chunk):
+    """perm(S_45) (tools/schur45.py, profiles/r2_schur45.json): the committed run's chunk
+    residues with one chunk removed; the resumed call re-walks that chunk (2^38 Glynn
+    indices, ~20 s) and must reproduce the recorded residues and the integer."""
+    import json
+    import os
+    src = os.path.join(os.path.dirname(__file__), "golden", f"schur45_{tag}_chunks.jsonl")
+    with open(src) as f:
+        lines = [json.loads(x) for x in f if x.strip()]
+    header = lines[0]["header"]
+    recorded = {r["chunk"]: r["residues"] for r in lines[1:]}
+    assert sorted(recorded) == list(range(64))
+    ck = tmp_path / "s45.jsonl"
+    with open(ck, "w") as f:
+        for rec in lines:
+            if rec.get("chunk") != chunk:
+                f.write(json.dumps(rec) + "\n")
+    basis = modular.CrtBasis(45, tuple(header["primes"]), math.prod(header["primes"]))
+    v, _, _, done = modular.schur_permanent_resumable(45, str(ck), chunks=64, basis=basis)
+    assert done == 64 and v == -470483360490107435783203125
+    with open(ck) as f:
+        redo = [json.loads(x) for x in f if '"chunk"' in x][-1]
+    assert redo == {"chunk": chunk, "residues": recorded[chunk]}
+
+
 def test_schur_resumable_rank_files(gpu, tmp_path):
     """Two scheduler-given ranks on one GPU, exchanging finished chunks through their files."""
     ck = str(tmp_path / "s25.jsonl")
