@@ -6,6 +6,8 @@ Under torchrun each rank walks chunks c = rank (mod world) on its own GPU
 (set_device_base(LOCAL_RANK)), writes s45_*.jsonl.rank<r>, and the residues are
 gathered over a gloo group; a rerun with any world size resumes from all the files.
 The paper projects ~28 GPU-hours for n = 45.
+$S45_N picks another odd n (a quick multi-rank check: S45_N=33 PK_LOGICAL_DEVICES=2
+torchrun --nproc-per-node 2 ... runs two ranks on one GPU, each on its own context).
 """
 import json
 import os
@@ -16,12 +18,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_10141_b200 import _native, modular  # noqa: E402
 
 CKDIR = os.environ.get("S45_CKDIR", "gpurun_out")  # copy checkpoints here to resume a cut run
+N = int(os.environ.get("S45_N", "45"))
 CHUNKS = 64  # 2^44 / 64 = 2^38 Glynn indices per chunk: 8 ranks get 8 chunks each
 
 
 def run(tag, basis):
     t0 = time.perf_counter()
-    v, b, w, done = modular.schur_permanent_resumable(45, os.path.join(CKDIR, f"s45_{tag}.jsonl"),
+    v, b, w, done = modular.schur_permanent_resumable(N, os.path.join(CKDIR, f"s{N}_{tag}.jsonl"),
                                                       chunks=CHUNKS, basis=basis)
     return {"basis": list(b.primes), "value": str(v), "chunks_done": done,
             "residues": [x.residue for x in w] if w else None,
@@ -35,14 +38,15 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo")
         _native.set_device_base(int(os.environ.get("LOCAL_RANK", "0")))
-    out = {"n": 45, "expansion": "glynn"}
-    out["fast"] = run("fast", modular.gpu_prime_basis(45))
+    out = {"n": N, "expansion": "glynn", "world": world}
+    out["fast"] = run("fast", modular.gpu_prime_basis(N))
     print(json.dumps(out["fast"]), flush=True)
-    out["check31"] = run("check31", modular.find_primes(45, max_bits=31))
+    out["check31"] = run("check31", modular.find_primes(N, max_bits=31))
     print(json.dumps(out["check31"]), flush=True)
     out["agree"] = out["fast"]["value"] == out["check31"]["value"]
     if int(os.environ.get("RANK", "0")) == 0:
-        with open("gpurun_out/schur45.json", "w") as f:
+        with open(f"gpurun_out/schur{N}_w{world}.json" if N != 45 else "gpurun_out/schur45.json",
+                  "w") as f:
             json.dump(out, f, indent=1)
         print("agree:", out["agree"])
 
