@@ -97,3 +97,37 @@ def test_reference_pinned_large_schur_values_consistent():
             assert v % p == r
             assert g == modular.primitive_nth_root(p, n)
         assert v % 2 == 1 and abs(v) <= n ** (n / 2)
+
+
+@pytest.mark.parametrize("n,value", [(45, -470483360490107435783203125),
+                                     (47, -52876272639843868105982022705)])
+def test_schur_long_run_chunk_records(n, value):
+    """The committed chunk residues of the perm(S_45) and perm(S_47) runs (tools/schur45.py):
+    the chunks of each basis add up (mod p, Glynn's 2^(1-n) applied) to residues whose CRT
+    lift is the recorded integer, and every extra-prime / second-basis record agrees."""
+    import glob
+    import json
+    import math
+    import os
+
+    from paper_2602_10141_b200 import modular
+    files = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", f"schur{n}_*_chunks.jsonl")))
+    assert len(files) == 2
+    for path in files:
+        with open(path) as f:
+            lines = [json.loads(x) for x in f if x.strip()]
+        recs = [r for r in lines if "chunk" in r]
+        assert sorted(r["chunk"] for r in recs) == list(range(64))
+        if "header" in lines[0]:
+            primes = lines[0]["header"]["primes"]
+            tot = [sum(r["residues"][k] for r in recs) for k in range(len(primes))]
+            wit = [modular.ResidueWitness(prime=p, root=0,
+                                          residue=modular._schur_finish(n, t, p, "glynn"))
+                   for p, t in zip(primes, tot)]
+            basis = modular.CrtBasis(n, tuple(primes), math.prod(primes))
+            assert modular.crt_reconstruct(wit, basis) == value
+        else:  # one extra prime, named in the file
+            q = int(path.rsplit("_q", 1)[1].split("_")[0])
+            r = modular._schur_finish(n, sum(x["residue"] for x in recs), q, "glynn")
+            assert r == value % q
+    assert value % n == 0
