@@ -49,7 +49,15 @@ __device__ __forceinline__ void neumaier_ref(double& s, double& c, double v) {
 }
 
 // steps in flight per thread (block_f64_kernel / block_modp_kernel skewed passes)
-constexpr int block_skew(bool cplx, int nmax) { return !cplx ? 4 : nmax >= 64 ? 1 : nmax >= 48 ? 2 : 4; }
+#ifndef PK_BLOCK_SKEW_REAL
+#define PK_BLOCK_SKEW_REAL 4
+#endif
+#ifndef PK_BLOCK_SKEW_CPLX
+#define PK_BLOCK_SKEW_CPLX 4
+#endif
+constexpr int block_skew(bool cplx, int nmax) {
+  return !cplx ? PK_BLOCK_SKEW_REAL : nmax >= 64 ? 1 : nmax >= 48 ? 2 : PK_BLOCK_SKEW_CPLX;
+}
 
 __device__ __forceinline__ int ctz64(uint64_t x) { return __ffsll(static_cast<long long>(x)) - 1; }
 
