@@ -6,6 +6,7 @@ Under torchrun each rank walks chunks c = rank (mod world) on its own GPU
 (set_device_base(LOCAL_RANK)), writes s45_*.jsonl.rank<r>, and the residues are
 gathered over a gloo group; a rerun with any world size resumes from all the files.
 The paper projects ~28 GPU-hours for n = 45.
+$S45_CHECK=59 checks on the reference's default 59-bit basis (Montgomery-64 walks);
 $S45_CHECK=prime replaces the second full basis by one extra 31-bit prime q outside the
 first basis (chunked and checkpointed too): value mod q must equal the walked residue.
 $S45_N picks another odd n (a quick multi-rank check: S45_N=33 PK_LOGICAL_DEVICES=2
@@ -73,13 +74,18 @@ def main():
         out["check_prime"] = check_prime(q, int(out["fast"]["value"]))
         print(json.dumps(out["check_prime"]), flush=True)
         out["agree"] = out["check_prime"]["agree"]
+    elif os.environ.get("S45_CHECK") == "59":  # the reference's default basis (modular.py:25)
+        out["check59"] = run("check59", modular.find_primes(N, max_bits=59))
+        print(json.dumps(out["check59"]), flush=True)
+        out["agree"] = out["fast"]["value"] == out["check59"]["value"]
     else:
         out["check31"] = run("check31", modular.find_primes(N, max_bits=31))
         print(json.dumps(out["check31"]), flush=True)
         out["agree"] = out["fast"]["value"] == out["check31"]["value"]
     if int(os.environ.get("RANK", "0")) == 0:
-        with open(f"gpurun_out/schur{N}_w{world}.json" if N != 45 else "gpurun_out/schur45.json",
-                  "w") as f:
+        tag = os.environ.get("S45_CHECK", "")
+        with open(f"gpurun_out/schur{N}_w{world}{'_' + tag if tag else ''}.json"
+                  if (N != 45 or tag) else "gpurun_out/schur45.json", "w") as f:
             json.dump(out, f, indent=1)
         print("agree:", out["agree"])
 
