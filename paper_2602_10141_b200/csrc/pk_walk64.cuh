@@ -119,6 +119,62 @@ __device__ __forceinline__ uint64_t redc64_cios(uint64_t x, uint64_t y, uint64_t
   return r;
 }
 
+// Lazy-walk REDC (p < 2^60, x, y < 4p < 2^62), word-serial like redc64_cios but
+// with the 64-bit column sums kept in IMAD.WIDE addends, which the bounds allow:
+//   mid = x0 y1 + x1 y0 < 2^63, A = mid + m0 p1 < 2^63.2 (p1 < 2^28), and
+//   digit 0 of T + m0 p is lo_lo + lo32(m0 p0) = 0 or 2^32: its carry is
+//   (lo_lo != 0), so only hi32(m0 p0) is formed (IMAD.HI, same cost as a wide).
+//   U = (T + m0 p) / 2^32 = S + hi 2^32, S = A + lo_hi + hi32(m0 p0) + c0 < 2^64;
+//   result = (U + m1 p) / 2^32 = (m1 p1 + hi) + hi32(S) + hi32(m1 p0) + c1.
+// Same fmaheavy cost as CIOS (6 IMAD.WIDE + 2 IMAD.HI + 2 IMAD), 10 carry adds
+// instead of 15.  Output in [0, 2p) for x y < p 2^64.  Measured +5-6 % over
+// CIOS at n = 35 / 36 (0.69 -> 0.73e12 prime-row-updates/s,
+// profiles/r2_redc_ps.txt): the default for the lazy walk; CIOS stays for
+// 2^60 <= p < 2^62, where the column sums would overflow.
+#ifndef PK_REDC64_PS
+#define PK_REDC64_PS 1
+#endif
+__device__ __forceinline__ uint64_t redc64_ps(uint64_t x, uint64_t y, uint64_t p,
+                                              uint64_t pinv) {
+  uint64_t r;
+  asm("{\n\t"
+      ".reg .u32 x0, x1, y0, y1, p0, p1, q0, q1, m0, m1, l0, l1, h0, h1, z, s0, s1, r0, r1;\n\t"
+      ".reg .u64 lo, A, hi, R;\n\t"
+      "mov.b64 {x0, x1}, %1;\n\t"
+      "mov.b64 {y0, y1}, %2;\n\t"
+      "mov.b64 {p0, p1}, %3;\n\t"
+      "mov.b64 {q0, q1}, %4;\n\t"
+      "neg.s32 q0, q0;\n\t"  // -p^-1 mod 2^32 from the positive inverse
+      "mul.wide.u32 lo, x0, y0;\n\t"
+      "mul.wide.u32 A, x0, y1;\n\t"
+      "mad.wide.u32 A, x1, y0, A;\n\t"
+      "mul.wide.u32 hi, x1, y1;\n\t"
+      "mov.b64 {l0, l1}, lo;\n\t"
+      "mul.lo.u32 m0, l0, q0;\n\t"
+      "mad.wide.u32 A, m0, p1, A;\n\t"
+      "mul.hi.u32 h0, m0, p0;\n\t"
+      "mov.b64 {s0, s1}, A;\n\t"
+      "add.cc.u32 z, l0, 0xffffffff;\n\t"  // carry = (l0 != 0)
+      "addc.cc.u32 s0, s0, l1;\n\t"
+      "addc.u32 s1, s1, 0;\n\t"
+      "add.cc.u32 s0, s0, h0;\n\t"
+      "addc.u32 s1, s1, 0;\n\t"
+      "mul.lo.u32 m1, s0, q0;\n\t"
+      "mad.wide.u32 R, m1, p1, hi;\n\t"
+      "mul.hi.u32 h1, m1, p0;\n\t"
+      "mov.b64 {r0, r1}, R;\n\t"
+      "add.cc.u32 z, s0, 0xffffffff;\n\t"  // carry = (s0 != 0)
+      "addc.cc.u32 r0, r0, s1;\n\t"
+      "addc.u32 r1, r1, 0;\n\t"
+      "add.cc.u32 r0, r0, h1;\n\t"
+      "addc.u32 r1, r1, 0;\n\t"
+      "mov.b64 %0, {r0, r1};\n\t"
+      "}"
+      : "=l"(r)
+      : "l"(x), "l"(y), "l"(p), "l"(pinv));
+  return r;
+}
+
 __device__ __forceinline__ uint64_t redc64_lazy(uint64_t x, uint64_t y, uint64_t p,
                                                 uint64_t pinv) {
   if constexpr (PK_REDC64_CIOS) return redc64_cios(x, y, p, pinv);
@@ -250,6 +306,10 @@ struct Modp64Walker {
   uint64_t acc_lo[P], acc_hi[P];  // exact 128-bit sum of the segment's terms
 
   __device__ __forceinline__ uint64_t p(int q) const { return mc->p64[q]; }
+  __device__ __forceinline__ uint64_t redc(uint64_t x, uint64_t y, int q) const {
+    if constexpr (LAZY && PK_REDC64_PS) return redc64_ps(x, y, p(q), mc->pinv64[q]);
+    return redc64_lazy(x, y, p(q), mc->pinv64[q]);
+  }
 
   __device__ __forceinline__ static void upd(uint64_t& r, uint64_t c, uint64_t p) {
     const uint64_t v = r + c;  // < 2p < 2^63
@@ -266,7 +326,7 @@ struct Modp64Walker {
         uint64_t v = r[q][j];
         int l = 0;
 #pragma unroll
-        for (; l < LOG && ((j >> l) & 1); ++l) v = redc64_lazy(st[l], v, p(q), mc->pinv64[q]);
+        for (; l < LOG && ((j >> l) & 1); ++l) v = redc(st[l], v, q);
         st[l] = v;
       }
       uint64_t acc = 0;
@@ -275,7 +335,7 @@ struct Modp64Walker {
       for (int l = 0; l < LOG; ++l) {
         if ((N >> l) & 1) {
           if (have) {
-            acc = redc64_lazy(st[l], acc, p(q), mc->pinv64[q]);
+            acc = redc(st[l], acc, q);
           } else {
             acc = st[l];
             have = true;
