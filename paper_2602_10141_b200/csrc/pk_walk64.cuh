@@ -128,11 +128,13 @@ __device__ __forceinline__ uint64_t redc64_cios(uint64_t x, uint64_t y, uint64_t
 //   result = (U + m1 p) / 2^32 = (m1 p1 + hi) + hi32(S) + hi32(m1 p0) + c1.
 // Same fmaheavy cost as CIOS (6 IMAD.WIDE + 2 IMAD.HI + 2 IMAD), 10 carry adds
 // instead of 15.  Output in [0, 2p) for x y < p 2^64.  Measured +5-6 % over
-// CIOS at n = 35 / 36 (0.69 -> 0.73e12 prime-row-updates/s,
-// profiles/r2_redc_ps.txt): the default for the lazy walk; CIOS stays for
+// CIOS at n = 35 / 36 (0.69 -> 0.73e12 prime-row-updates/s); form 2 folds the
+// 32-bit addend and digit 0's carry into the high product (madc.hi.cc: no
+// zeroed addend register per IMAD.HI), another +2 % (0.75e12,
+// profiles/r2_redc_ps.txt): the default for the lazy walk.  CIOS stays for
 // 2^60 <= p < 2^62, where the column sums would overflow.
 #ifndef PK_REDC64_PS
-#define PK_REDC64_PS 1
+#define PK_REDC64_PS 2
 #endif
 __device__ __forceinline__ uint64_t redc64_ps(uint64_t x, uint64_t y, uint64_t p,
                                               uint64_t pinv) {
@@ -152,8 +154,25 @@ __device__ __forceinline__ uint64_t redc64_ps(uint64_t x, uint64_t y, uint64_t p
       "mov.b64 {l0, l1}, lo;\n\t"
       "mul.lo.u32 m0, l0, q0;\n\t"
       "mad.wide.u32 A, m0, p1, A;\n\t"
-      "mul.hi.u32 h0, m0, p0;\n\t"
       "mov.b64 {s0, s1}, A;\n\t"
+#if PK_REDC64_PS == 2
+      // h0 = hi(m0 p0) + l1 + c0 in one extended-precision multiply-add; its
+      // carry has weight 2^32, i.e. goes straight into s1
+      "add.cc.u32 z, l0, 0xffffffff;\n\t"  // carry = (l0 != 0)
+      "madc.hi.cc.u32 h0, m0, p0, l1;\n\t"
+      "addc.u32 s1, s1, 0;\n\t"
+      "add.cc.u32 s0, s0, h0;\n\t"
+      "addc.u32 s1, s1, 0;\n\t"
+      "mul.lo.u32 m1, s0, q0;\n\t"
+      "mad.wide.u32 R, m1, p1, hi;\n\t"
+      "mov.b64 {r0, r1}, R;\n\t"
+      "add.cc.u32 z, s0, 0xffffffff;\n\t"  // carry = (s0 != 0)
+      "madc.hi.cc.u32 h1, m1, p0, s1;\n\t"
+      "addc.u32 r1, r1, 0;\n\t"
+      "add.cc.u32 r0, r0, h1;\n\t"
+      "addc.u32 r1, r1, 0;\n\t"
+#else
+      "mul.hi.u32 h0, m0, p0;\n\t"
       "add.cc.u32 z, l0, 0xffffffff;\n\t"  // carry = (l0 != 0)
       "addc.cc.u32 s0, s0, l1;\n\t"
       "addc.u32 s1, s1, 0;\n\t"
@@ -168,6 +187,7 @@ __device__ __forceinline__ uint64_t redc64_ps(uint64_t x, uint64_t y, uint64_t p
       "addc.u32 r1, r1, 0;\n\t"
       "add.cc.u32 r0, r0, h1;\n\t"
       "addc.u32 r1, r1, 0;\n\t"
+#endif
       "mov.b64 %0, {r0, r1};\n\t"
       "}"
       : "=l"(r)

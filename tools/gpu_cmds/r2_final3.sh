@@ -1,5 +1,5 @@
 #!/bin/bash
-# round 2 re-entry: product-scanning Montgomery-64 REDC adopted; wide parity first, then the
+# round 2 re-entry: column-sum Montgomery-64 REDC (PK_REDC64_PS) adopted; wide parity first, then the
 # full GPU suite, smoke, both bench arms, and the Montgomery-64 rates
 cd "$GRAFT_REPO_ROOT"
 mkdir -p gpurun_out
